@@ -1,0 +1,97 @@
+/*
+ * mag_b200.h — GPU additions to the mag.h ABI (libmag_b200.so).
+ *
+ * Nothing here changes the reference entry points in mag.h; these calls only
+ * expose what a GPU caller needs beyond them: text that already lives in HBM,
+ * stream-ordered (asynchronous) searches, the search plan the engine chose
+ * and a few introspection hooks used by the parity tests.
+ */
+#ifndef MAG_B200_H
+#define MAG_B200_H
+
+#include "mag.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Gram modes of the filter's q-gram stage. */
+typedef enum mag_gram_mode {
+  MAG_GRAM_AUTO = -1,
+  MAG_GRAM_EXACT = 0,  /* reference code: sum map(p[i]) * sigma'^i, sigma'^q entries */
+  MAG_GRAM_HASHED = 1  /* raw q bytes hashed to 2^table_bits entries (paper §3.3) */
+} mag_gram_mode;
+
+/* Extended options.  mag_engine_create(opts) == mag_engine_create_ex with
+ * every extra field left at its default. */
+typedef struct mag_options_ex {
+  mag_options base;
+  int gram_mode;   /* mag_gram_mode */
+  int table_bits;  /* hashed: log2 mask entries; 0 = auto; -1 = no filter (verify all) */
+  int word_bits;   /* w of the reference machine (filter.hpp:34); 0 = 64 */
+  int tile_bytes;  /* 0 = auto */
+  int warps;       /* consumer warps per CTA, 0 = auto (<= 16) */
+  int stages;      /* TMA ring depth, 0 = auto */
+  int device;      /* CUDA device ordinal, -1 = current */
+} mag_options_ex;
+
+MAG_API void mag_options_ex_init(mag_options_ex* opts);
+MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns,
+                                        const size_t* pattern_lens, size_t count,
+                                        const mag_options_ex* opts, mag_engine** out);
+
+/* The plan the engine runs (all fields are what the kernels use). */
+typedef struct mag_plan_info {
+  int variant;          /* mag_variant */
+  int gram_mode;        /* mag_gram_mode in effect */
+  int q, k, m_prime;
+  int sigma_prime;
+  int verify_all;       /* 1: the table admits everything; every start is verified */
+  uint32_t table_bits;  /* hashed: log2 entries */
+  uint32_t entry_bits;  /* bits per mask entry */
+  uint64_t table_bytes;
+  int table_in_smem;
+  uint32_t key_len;     /* verification key bytes */
+  uint32_t prefilter_bits;
+  uint32_t bucket_bits;
+  uint32_t tile_bytes, halo, warps, stages;
+  size_t smem_bytes;
+  double predicted_candidates_per_byte;
+} mag_plan_info;
+
+MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);
+
+/* Text already in device memory (caller-owned, must outlive the handle). */
+MAG_API mag_status mag_prepare_device_text(const mag_engine* engine, const uint8_t* d_text,
+                                           size_t len, mag_prepared** out);
+
+/* Enqueue a search on `cuda_stream` (a cudaStream_t; NULL = legacy default)
+ * and return at once.  The handle materialises (waits, copies the sorted
+ * matches to the host) on first use by mag_matches_count/get/metrics or by
+ * mag_matches_sync; destroying it unmaterialised is allowed. */
+MAG_API mag_status mag_search_prepared_async(const mag_engine* engine,
+                                             const mag_prepared* prepared, void* cuda_stream,
+                                             mag_matches** out);
+MAG_API mag_status mag_matches_sync(mag_matches* matches);
+
+/* Bulk read of the sorted matches (after materialisation). */
+MAG_API mag_status mag_matches_copy(const mag_matches* matches, uint64_t* offsets,
+                                    uint32_t* pattern_indices, size_t capacity);
+
+/* Introspection for tests. */
+MAG_API mag_status mag_prepared_copy_codes(const mag_prepared* prepared, uint32_t* out,
+                                           size_t count);
+MAG_API mag_status mag_engine_copy_masks(const mag_engine* engine, uint64_t* out,
+                                         size_t count);
+MAG_API uint64_t mag_kernel_launches(void);
+
+/* Device timing of the fused scan kernel: when enabled, every scan launch is
+ * bracketed by CUDA events on its stream; read() waits for and sums them. */
+MAG_API void mag_scan_timer_enable(int on);
+MAG_API mag_status mag_scan_timer_read(double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAG_B200_H */

@@ -1,0 +1,639 @@
+// Host model of the search (see host_model.h).  Reference citations are
+// /root/reference paths.
+#include "host_model.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+namespace magb {
+
+// ------------------------------------------------------------------ maps
+// alphabet_map.cpp:42-50: bytes by descending count, ties by ascending byte.
+static void rank_bytes(const Histogram& h, int order[256]) {
+  for (int i = 0; i < 256; ++i) order[i] = i;
+  std::stable_sort(order, order + 256, [&](int a, int b) { return h.counts[a] > h.counts[b]; });
+}
+
+bool build_map(int strategy, const Histogram& h, uint32_t sigma_prime, unsigned lowbits,
+               uint8_t table[256], uint32_t* sigma_out, std::string* err) {
+  int order[256];
+  auto bad_sigma = [&]() {
+    if (sigma_prime < 2 || sigma_prime > 256) {
+      *err = "sigma' must be in [2, 256], got " + std::to_string(sigma_prime);
+      return true;
+    }
+    return false;
+  };
+  switch (strategy) {
+    case kMapIdentity:
+      for (int c = 0; c < 256; ++c) table[c] = static_cast<uint8_t>(c);
+      *sigma_out = 256;
+      return true;
+    case kMapFrequency:  // alphabet_map.cpp:78-88
+      if (bad_sigma()) return false;
+      rank_bytes(h, order);
+      for (uint32_t rank = 0; rank < 256; ++rank)
+        table[order[rank]] = static_cast<uint8_t>(rank < sigma_prime - 1 ? rank : sigma_prime - 1);
+      *sigma_out = sigma_prime;
+      return true;
+    case kMapBalanced: {  // alphabet_map.cpp:90-102 (greedy LPT, ties to lowest bin)
+      if (bad_sigma()) return false;
+      rank_bytes(h, order);
+      std::vector<uint64_t> load(sigma_prime, 0);
+      for (int i = 0; i < 256; ++i) {
+        uint32_t best = static_cast<uint32_t>(std::min_element(load.begin(), load.end()) - load.begin());
+        table[order[i]] = static_cast<uint8_t>(best);
+        load[best] += h.counts[order[i]];
+      }
+      *sigma_out = sigma_prime;
+      return true;
+    }
+    case kMapLowbits:  // alphabet_map.cpp:104-114
+      if (lowbits < 1 || lowbits > 8) {
+        *err = "lowbits bit count must be in [1, 8], got " + std::to_string(lowbits);
+        return false;
+      }
+      for (unsigned c = 0; c < 256; ++c) table[c] = static_cast<uint8_t>(c & ((1u << lowbits) - 1));
+      *sigma_out = 1u << lowbits;
+      return true;
+  }
+  *err = "unknown mapping strategy " + std::to_string(strategy);
+  return false;
+}
+
+// ----------------------------------------------------------------- tuner
+// Restated from tuner.hpp:30-66 and SPEC.md:427-492; kept bit-identical to
+// oracle/mag_oracle.c mo_tune().
+double expected_class_size(double sigma_eff, double n_super) {
+  if (sigma_eff <= 0) return 0;
+  return sigma_eff * (1.0 - std::pow(1.0 - 1.0 / sigma_eff, n_super));
+}
+
+double match_probability(double sigma_eff, double n_super) {
+  if (sigma_eff <= 0) return 1;
+  return 1.0 - std::pow(1.0 - 1.0 / sigma_eff, n_super);
+}
+
+uint32_t resolve_sigma_prime(uint32_t sigma_observed, uint32_t user_choice) {
+  if (user_choice) return user_choice;
+  if (sigma_observed <= 64) return sigma_observed < 2 ? 2 : sigma_observed;
+  return 256;
+}
+
+static double log_base(double x, double b) { return std::log(x) / std::log(b); }
+
+static bool q_feasible(uint32_t sp, uint64_t m, unsigned q) {
+  if (q < 1 || q > 8) return false;
+  if (m < 2ull * q - 1) return false;
+  return std::pow(static_cast<double>(sp), static_cast<double>(q)) <= static_cast<double>(1u << 24);
+}
+
+unsigned choose_q(const TuningInput& ti) {
+  const double rm = static_cast<double>(ti.r) * static_cast<double>(ti.m);
+  const double lq = rm > 1 ? log_base(rm, ti.sigma_prime) : 0;
+  long q = std::lround(lq);
+  q = std::clamp<long>(q, 1, 8);
+  while (q > 1 && !q_feasible(ti.sigma_prime, ti.m, static_cast<unsigned>(q))) --q;
+  return static_cast<unsigned>(q);
+}
+
+double strided_k_seed(const TuningInput& ti, unsigned /*q*/) {
+  const double rm = static_cast<double>(ti.r) * static_cast<double>(ti.m);
+  const double L = log_base(rm, ti.sigma_prime);
+  if (L <= 0) return 1;
+  const double rho = L / static_cast<double>(ti.m);
+  const double l = log_base(1.0 / rho, ti.sigma_prime);
+  if (L + l <= 0) return 1;
+  return static_cast<double>(ti.m) / L * l / (L + l);
+}
+
+static unsigned alignment_len(const TuningInput& ti, unsigned q, unsigned k) {
+  const uint64_t Lq = (ti.m - q + 1) / q;
+  const unsigned w = ti.word_bits ? ti.word_bits : 64;
+  return static_cast<unsigned>(std::min<uint64_t>(Lq / k, w / k));
+}
+
+double predicted_cost(const TuningInput& ti, unsigned q, unsigned k) {
+  const double nq = static_cast<double>(ti.n / q);
+  const double p = match_probability(std::pow(static_cast<double>(ti.sigma_prime), q),
+                                     static_cast<double>(q) * static_cast<double>(ti.r));
+  const unsigned mp = alignment_len(ti, q, k);
+  return nq / k + nq * std::pow(p, mp) * (2.0 * q - 1) * static_cast<double>(ti.r) *
+                      static_cast<double>(ti.m);
+}
+
+unsigned choose_k(const TuningInput& ti, unsigned q) {
+  const uint64_t Lq = std::max<uint64_t>(1, (ti.m - q + 1) / q);
+  const unsigned w = ti.word_bits ? ti.word_bits : 64;
+  long k0 = std::lround(strided_k_seed(ti, q));
+  k0 = std::clamp<long>(k0, 1, static_cast<long>(Lq));
+  const long lo = std::max<long>(1, k0 - 2), hi = std::min<long>(static_cast<long>(Lq), k0 + 2);
+  unsigned best = static_cast<unsigned>(k0);
+  double bc = std::numeric_limits<double>::infinity();
+  for (long k = lo; k <= hi; ++k) {
+    if (static_cast<unsigned>(k) > w) continue;
+    const double c = predicted_cost(ti, q, static_cast<unsigned>(k));
+    if (c < bc) {
+      bc = c;
+      best = static_cast<unsigned>(k);
+    }
+  }
+  return best;
+}
+
+bool tune(const TuningInput& in, int fixed_q, int fixed_k, TuningResult* out, std::string* err) {
+  TuningInput ti = in;
+  if (ti.r < 1 || ti.m < 1 || ti.sigma < 1) {
+    *err = "tuning input needs r, m, sigma >= 1";
+    return false;
+  }
+  if (!ti.word_bits) ti.word_bits = 64;
+  ti.sigma_prime = resolve_sigma_prime(ti.sigma, ti.sigma_prime);
+  if (ti.sigma_prime < 2 || ti.sigma_prime > 256) {
+    *err = "sigma' must be in [2, 256]";
+    return false;
+  }
+  const unsigned q0 = fixed_q > 0 ? static_cast<unsigned>(fixed_q) : choose_q(ti);
+  if (!q_feasible(ti.sigma_prime, ti.m, q0)) {
+    *err = "q = " + std::to_string(q0) + " is infeasible (q <= 8, sigma'^q <= 2^24, m >= 2q-1)";
+    return false;
+  }
+  unsigned qlo = q0, qhi = q0;
+  if (fixed_q <= 0) {  // tuner.hpp:63-64 joint local grid around the seeds
+    qlo = q0 > 2 ? q0 - 2 : 1;
+    qhi = q0 + 2;
+  }
+  unsigned bq = q0, bk = 1;
+  double bc = std::numeric_limits<double>::infinity();
+  for (unsigned q = qlo; q <= qhi; ++q) {
+    if (!q_feasible(ti.sigma_prime, ti.m, q)) continue;
+    unsigned k;
+    if (fixed_k > 0) {
+      const uint64_t Lq = (ti.m - q + 1) / q;
+      if (static_cast<uint64_t>(fixed_k) > Lq || static_cast<unsigned>(fixed_k) > ti.word_bits)
+        continue;
+      k = static_cast<unsigned>(fixed_k);
+    } else {
+      k = choose_k(ti, q);
+    }
+    const double c = predicted_cost(ti, q, k);
+    if (c < bc) {
+      bc = c;
+      bq = q;
+      bk = k;
+    }
+  }
+  if (!std::isfinite(bc)) {
+    *err = "no feasible (q, k)";
+    return false;
+  }
+  const double rm = static_cast<double>(ti.r) * static_cast<double>(ti.m);
+  out->q = bq;
+  out->k = bk;
+  out->sigma_prime = ti.sigma_prime;
+  out->rho = (rm > 1 ? log_base(rm, ti.sigma_prime) : 0) / static_cast<double>(ti.m);
+  out->predicted_p = match_probability(std::pow(static_cast<double>(ti.sigma_prime), bq),
+                                       static_cast<double>(bq) * static_cast<double>(ti.r));
+  out->predicted_cost = bc;
+  return true;
+}
+
+// ------------------------------------------------------------------ plan
+namespace {
+
+constexpr uint32_t kDefaultTile = 8192;
+constexpr uint32_t kDefaultStages = 4;
+constexpr uint32_t kDefaultWarps = 16;
+constexpr uint32_t kMbuf = 32;
+
+unsigned pow2ceil_log2(unsigned x) {
+  unsigned l = 0;
+  while ((1u << l) < x) ++l;
+  return l;
+}
+
+// Probability that a text gram hits an admitted entry at one class position:
+// exact membership (uniform text over the pattern alphabet) plus hash
+// collisions into 2^table_bits entries.
+double est_position_p(double admissions, double universe, double entries) {
+  double distinct, exact;
+  if (universe > 1e15) {
+    distinct = admissions;
+    exact = 0;
+  } else {
+    distinct = universe * (1.0 - std::exp(-admissions / universe));
+    exact = distinct / universe;
+  }
+  if (entries <= 1) return 1.0;
+  const double coll = 1.0 - std::exp(-distinct / entries);
+  return exact + (1.0 - exact) * coll;
+}
+
+double prefilter_fp(double keys, unsigned pf_bits) {
+  const double f = 1.0 - std::exp(-2.0 * keys / std::ldexp(1.0, static_cast<int>(pf_bits)));
+  return f * f;
+}
+
+// Cost model in thread-instructions per text byte (calibrated on B200, see
+// DESIGN.md): per sample gram+lookup, per extra m' a shuffle, per candidate
+// a queue slot, per verified start a rolled key + prefilter, per prefilter
+// pass an L2 bucket probe.
+constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 12,
+                 kCostProbe = 150, kCostVerifyAll = 16;
+
+uint32_t gcd32(uint32_t a, uint32_t b) {
+  while (b) {
+    uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
+  ScanPlan& sp = P->sp;
+  const uint32_t gs = sp.overlapping ? 1 : sp.q;
+  const uint32_t step = 16 / gcd32(16, gs) * gs;  // lcm(16, gram step)
+  uint32_t tile = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes) : kDefaultTile;
+  tile = std::max(step, tile / step * step);
+  P->tile_bytes = tile;
+  const uint64_t reach = sp.verify_all ? 16 : static_cast<uint64_t>(gs) * sp.k * sp.m_prime + sp.q;
+  const uint64_t verify_reach = std::min<uint64_t>(pd.maxlen, 1024);
+  P->halo = static_cast<uint32_t>(align16(std::max<uint64_t>(reach, verify_reach) + 32));
+  P->stages = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultStages;
+  P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kDefaultWarps;
+  P->mbuf = kMbuf;
+}
+
+size_t fixed_smem(const Plan& P) {
+  ScanPlan z = P.sp;
+  z.table_in_smem = 0;
+  z.pf_bits = 0;
+  return smem_layout(z, P.tile_bytes, P.halo, P.stages, P.nwarps, P.mbuf).total;
+}
+
+void set_entry_geometry(ScanPlan& sp) {
+  const unsigned bits = sp.k * sp.m_prime;
+  sp.entry_log2 = pow2ceil_log2(std::max(1u, bits));
+  uint64_t match = 0;
+  for (unsigned j = 0; j < sp.k; ++j) match |= 1ull << (j * sp.m_prime + sp.m_prime - 1);
+  sp.match_mask = match;
+  const uint64_t tbits = sp.entries << sp.entry_log2;
+  sp.table_bytes = align16(std::max<uint64_t>(16, (tbits + 7) / 8));
+}
+
+}  // namespace
+
+int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, Plan* P,
+              std::string* err) {
+  constexpr int kOk = 0, kBadConfig = 5;
+  *P = Plan{};
+  ScanPlan& sp = P->sp;
+  P->variant = rq.variant;
+  if (rq.variant == 3 || rq.variant == 4) {
+    *err = "variants naive/ac are CPU oracles; this GPU library runs mag, smag and shiftor_og";
+    return kBadConfig;
+  }
+  if (rq.variant < 0 || rq.variant > 4) {
+    *err = "unknown variant " + std::to_string(rq.variant);
+    return kBadConfig;
+  }
+  if (pd.r > kMaxPatterns) {
+    *err = "at most 2^24 patterns are supported";
+    return kBadConfig;
+  }
+  sp.overlapping = rq.variant == 2;
+  sp.smag = rq.variant == 1;
+  sp.m = static_cast<uint32_t>(std::min<size_t>(pd.m, 0xffffffffu));
+  sp.maxlen = static_cast<uint32_t>(std::min<size_t>(pd.maxlen, 0xffffffffu));
+  sp.r = static_cast<uint32_t>(pd.r);
+  sp.key_len = static_cast<uint32_t>(std::min<size_t>(pd.m, 16));
+  {
+    uint32_t pw = 1;
+    for (uint32_t i = 1; i < sp.key_len; ++i) pw *= kKeyBase;
+    sp.key_pow = pw;
+  }
+  const uint32_t sigma_obs = std::max(1u, h.distinct());
+  const size_t m = pd.m;
+  const unsigned w = rq.word_bits > 0 ? std::min(64, rq.word_bits) : 64;
+
+  const bool reference_mode = rq.gram_mode == 0 ||
+                              (rq.gram_mode < 0 && (rq.q || rq.k || rq.sigma_prime ||
+                                                     rq.mapping != -1));
+  if (reference_mode) {
+    // ---- the reference engine's own parameter path (engine.hpp:22-33)
+    sp.gram_mode = kGramExact;
+    int mapping = rq.mapping;
+    uint32_t sigma_req = static_cast<uint32_t>(std::max(0, rq.sigma_prime));
+    uint32_t sprime = resolve_sigma_prime(sigma_obs, sigma_req);
+    if (mapping == -1) mapping = sprime < 256 ? kMapBalanced : kMapIdentity;  // mag.h:47
+    uint32_t sp_out = 0;
+    if (!build_map(mapping, h, sprime, static_cast<unsigned>(std::max(0, rq.lowbits)), P->map,
+                   &sp_out, err))
+      return kBadConfig;
+    P->mapping = mapping;
+    sp.sigma_prime = sp_out;
+    TuningInput ti;
+    ti.sigma = sigma_obs;
+    ti.sigma_prime = sp_out;
+    ti.r = pd.r;
+    ti.m = m;
+    ti.word_bits = w;
+    unsigned q = rq.q > 0 ? static_cast<unsigned>(rq.q) : 0;
+    unsigned k = rq.k > 0 ? static_cast<unsigned>(rq.k) : 0;
+    if (!q || (!k && !sp.overlapping)) {
+      TuningResult tr;
+      std::string terr;
+      if (tune(ti, rq.q, sp.overlapping ? 1 : rq.k, &tr, &terr)) {
+        if (!q) q = tr.q;
+        if (!k) k = tr.k;
+      } else if (!q) {
+        q = 1;
+      }
+    }
+    if (sp.overlapping) k = 1;
+    if (!k) k = 1;
+    // GramConfig (qgram.cpp:9-19)
+    if (q < 1 || q > 8) {
+      *err = "q must be in [1, 8], got " + std::to_string(q);
+      return kBadConfig;
+    }
+    uint64_t space = 1;
+    for (unsigned i = 0; i < q; ++i) {
+      space *= sp_out;
+      if (space > (1u << 24)) {
+        *err = "sigma'^q exceeds the table budget (" + std::to_string(sp_out) + "^" +
+               std::to_string(q) + " > 2^24); lower q or reduce the alphabet";
+        return kBadConfig;
+      }
+    }
+    sp.entries = space;
+    sp.q = q;
+    sp.k = k;
+  } else {
+    // ---- GPU planner: hashed q-gram alphabet sized to shared memory
+    sp.gram_mode = kGramHashed;
+    P->mapping = kMapIdentity;
+    for (int c = 0; c < 256; ++c) P->map[c] = static_cast<uint8_t>(c);
+    sp.sigma_prime = 256;
+    Plan probe = *P;
+    probe.sp.q = 1;
+    probe.sp.k = 1;
+    probe.sp.m_prime = 1;
+    finish_geometry(pd, rq, &probe);
+    const size_t room = rq.smem_limit > fixed_smem(probe) + 4096
+                            ? rq.smem_limit - fixed_smem(probe) - 4096
+                            : 0;
+    const double keys = static_cast<double>(pd.r);
+    struct Cand {
+      double cost = std::numeric_limits<double>::infinity();
+      unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 7;
+      bool va = true;
+      double cpb = 1;
+    } best;
+    // verify-all baseline: whole room to the prefilter
+    {
+      unsigned pf = 7;
+      while (pf < 24 && (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
+      best.cost = kCostVerifyAll + prefilter_fp(keys, pf) * kCostProbe;
+      best.pf = pf;
+      best.cpb = 1;
+    }
+    if (rq.table_bits >= 0) {
+      const unsigned qmax = sp.overlapping ? static_cast<unsigned>(std::min<size_t>(16, m))
+                                           : static_cast<unsigned>(std::min<size_t>(16, (m + 1) / 2));
+      for (unsigned q = 1; q <= qmax; ++q) {
+        if (rq.q > 0 && q != static_cast<unsigned>(rq.q)) continue;
+        const size_t L = sp.overlapping ? m - q + 1 : (m - q + 1) / q;
+        if (L < 1) continue;
+        const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
+        const unsigned kmax = sp.overlapping ? 1 : static_cast<unsigned>(std::min<size_t>(L, w));
+        for (unsigned k = 1; k <= kmax; ++k) {
+          if (rq.k > 0 && !sp.overlapping && k != static_cast<unsigned>(rq.k)) continue;
+          const unsigned mpmax = static_cast<unsigned>(std::min<size_t>(L / k, w / k));
+          for (unsigned mp = 1; mp <= mpmax; ++mp) {
+            const unsigned el = pow2ceil_log2(std::max(1u, k * mp));
+            for (unsigned tbits = 14; tbits <= 24; ++tbits) {
+              const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
+              if (tbytes + 16 > room) break;
+              if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
+              unsigned pf = 7;
+              while (pf < 24 && tbytes + (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
+              const double adm = sp.overlapping ? keys : keys * q;
+              const double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
+              const double pm = std::pow(p, static_cast<double>(mp));
+              double cost, cpb;
+              if (sp.overlapping) {
+                cpb = pm;
+                cost = kCostSample + (mp - 1) * kCostShift +
+                       pm * (kCostCand + kCostStart + prefilter_fp(keys, pf) * kCostProbe);
+              } else {
+                cpb = pm / q;  // k alignments per sample, one sample per k*q bytes
+                cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) + cpb * kCostCand +
+                       pm * (kCostStart + prefilter_fp(keys, pf) * kCostProbe);
+              }
+              if (cost < best.cost * 0.999) {
+                best.cost = cost;
+                best.q = q;
+                best.k = k;
+                best.mp = mp;
+                best.tb = tbits;
+                best.pf = pf;
+                best.va = false;
+                best.cpb = cpb;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (best.va) {
+      sp.q = 1;
+      sp.k = 1;
+      sp.m_prime = 1;
+      sp.table_bits = 0;
+      sp.entries = 1;
+      sp.verify_all = 1;
+    } else {
+      sp.q = best.q;
+      sp.k = best.k;
+      sp.m_prime = best.mp;
+      sp.table_bits = best.tb;
+      sp.entries = 1ull << best.tb;
+    }
+    sp.pf_bits = best.pf;
+    P->pred_cand_per_byte = best.cpb;
+  }
+
+  // ---- machine shape (filter.hpp:27-31, superimpose.cpp:11-21)
+  const unsigned q = sp.q;
+  size_t L;
+  if (sp.overlapping) {
+    if (m < q) {
+      *err = "m = " + std::to_string(m) + " is shorter than q; lower q";
+      return kBadConfig;
+    }
+    L = m - q + 1;
+    sp.k = 1;
+  } else {
+    if (m < 2 * static_cast<size_t>(q) - 1) {
+      *err = "m = " + std::to_string(m) + " is below 2q-1 = " + std::to_string(2 * q - 1) +
+             "; lower q so every shift yields at least one gram";
+      return kBadConfig;
+    }
+    L = (m - q + 1) / q;
+  }
+  if (sp.k < 1 || sp.k > L || sp.k > w) {
+    *err = "k = " + std::to_string(sp.k) + " is infeasible for L = " + std::to_string(L) +
+           " and w = " + std::to_string(w);
+    return kBadConfig;
+  }
+  if (reference_mode || sp.m_prime == 0)
+    sp.m_prime = static_cast<uint32_t>(std::min<size_t>(L / sp.k, w / sp.k));
+  set_entry_geometry(sp);
+  finish_geometry(pd, rq, P);
+
+  // ---- shared-memory placement
+  const size_t fixed = fixed_smem(*P);
+  if (reference_mode) {
+    // prefilter first (>= 2^12 bits), then the table if it fits
+    unsigned pf = 12;
+    const size_t room = rq.smem_limit > fixed + 4096 ? rq.smem_limit - fixed - 4096 : 0;
+    sp.table_in_smem = sp.table_bytes + (size_t(1) << pf) / 8 <= room;
+    const size_t left = room - (sp.table_in_smem ? sp.table_bytes : 0);
+    while (pf < 22 && (size_t(1) << (pf + 1)) / 8 <= left &&
+           (size_t(1) << pf) < 16 * std::max<size_t>(pd.r, 1))
+      ++pf;
+    sp.pf_bits = pf;
+  } else {
+    sp.table_in_smem = sp.verify_all ? 0 : 1;
+  }
+  {
+    unsigned bb = 4;
+    while ((size_t(1) << bb) < 2 * pd.r && bb < 26) ++bb;
+    sp.bucket_bits = bb;
+  }
+  const size_t total = smem_layout(sp, P->tile_bytes, P->halo, P->stages, P->nwarps, P->mbuf).total;
+  if (total > rq.smem_limit) {
+    *err = "plan needs " + std::to_string(total) + " bytes of shared memory (limit " +
+           std::to_string(rq.smem_limit) + ")";
+    return kBadConfig;
+  }
+  return kOk;
+}
+
+// --------------------------------------------------------------- tables
+static inline uint32_t gram_index_host(const Plan& P, const uint8_t* g) {
+  const ScanPlan& sp = P.sp;
+  if (sp.gram_mode == kGramExact) {
+    uint32_t code = P.map[g[sp.q - 1]];
+    for (int i = static_cast<int>(sp.q) - 2; i >= 0; --i) code = code * sp.sigma_prime + P.map[g[i]];
+    return code;
+  }
+  return gram_slot(hash_gram_bytes(g, sp.q), sp.table_bits);
+}
+
+static inline void clear_bit(const Plan& P, std::vector<uint8_t>* t, uint64_t idx, unsigned b) {
+  const unsigned el = P.sp.entry_log2;
+  if (el == 6) {
+    uint64_t* w = reinterpret_cast<uint64_t*>(t->data());
+    w[idx] &= ~(1ull << b);
+  } else {
+    uint32_t* w = reinterpret_cast<uint32_t*>(t->data());
+    const uint64_t wi = idx >> (5 - el);
+    const unsigned sh = static_cast<unsigned>((idx & ((32u >> el) - 1u)) << el);
+    w[wi] &= ~(1u << (sh + b));
+  }
+}
+
+uint64_t mask_entry(const Plan& P, const std::vector<uint8_t>& t, uint64_t idx) {
+  const unsigned el = P.sp.entry_log2;
+  if (el == 6) return reinterpret_cast<const uint64_t*>(t.data())[idx];
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(t.data());
+  const uint64_t wi = idx >> (5 - el);
+  const unsigned sh = static_cast<unsigned>((idx & ((32u >> el) - 1u)) << el);
+  const unsigned bits = 1u << el;
+  const uint64_t v = (w[wi] >> sh) & (bits == 32 ? 0xffffffffull : ((1ull << bits) - 1));
+  // widen: bits past the entry read as 1 (never admitted)
+  return v | (bits >= 64 ? 0 : (~0ull << bits));
+}
+
+// superimpose.hpp:33-47 admissions streamed into masks (filter.hpp:27-31):
+// class position c goes to alignment c % k, position c / k (P^j[i]=P[j+ik]).
+void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* table) {
+  const ScanPlan& sp = P.sp;
+  table->assign(sp.table_bytes, 0xff);
+  if (sp.verify_all) {
+    table->assign(sp.table_bytes, 0);
+    return;
+  }
+  const size_t m = pd.m;
+  const unsigned q = sp.q;
+  const size_t L = sp.overlapping ? m - q + 1 : (m - q + 1) / q;
+  const unsigned shifts = sp.overlapping ? 1 : q;
+  for (size_t i = 0; i < pd.r; ++i) {
+    const uint8_t* p = pd.pattern(i);
+    for (unsigned s = 0; s < shifts; ++s) {
+      for (size_t c = 0; c < L; ++c) {
+        const size_t align = c % sp.k, pos = c / sp.k;
+        if (pos >= sp.m_prime) continue;
+        const uint8_t* g = sp.overlapping ? p + c : p + s + c * q;
+        clear_bit(P, table, gram_index_host(P, g),
+                  static_cast<unsigned>(align * sp.m_prime + pos));
+      }
+    }
+  }
+}
+
+void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt) {
+  const ScanPlan& sp = P.sp;
+  const size_t r = pd.r;
+  std::vector<uint32_t> keys(r);
+  for (size_t i = 0; i < r; ++i) keys[i] = key_mix(key_poly(pd.pattern(i), sp.key_len));
+  // prefilter: two probes per key (scan_kernels.cu prefilter_pass)
+  const size_t pf_words = std::max<size_t>(4, (size_t(1) << sp.pf_bits) / 32);
+  pt->prefilter.assign(align16(pf_words * 4) / 4, 0);
+  for (size_t i = 0; i < r; ++i) {
+    const uint32_t key = keys[i];
+    const uint32_t i1 = key >> (32 - sp.pf_bits);
+    const uint32_t i2 = ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - sp.pf_bits);
+    pt->prefilter[i1 >> 5] |= 1u << (i1 & 31);
+    pt->prefilter[i2 >> 5] |= 1u << (i2 & 31);
+  }
+  // buckets by low key bits; entries ordered by (bucket, pattern index)
+  const size_t nb = size_t(1) << sp.bucket_bits;
+  pt->bucket_start.assign(nb + 1, 0);
+  for (size_t i = 0; i < r; ++i) pt->bucket_start[(keys[i] & (nb - 1)) + 1]++;
+  for (size_t b = 0; b < nb; ++b) pt->bucket_start[b + 1] += pt->bucket_start[b];
+  std::vector<uint32_t> cursor(pt->bucket_start.begin(), pt->bucket_start.end() - 1);
+  pt->entries.assign(2 * std::max<size_t>(r, 1), 0);
+  for (size_t i = 0; i < r; ++i) {
+    const uint32_t e = cursor[keys[i] & (nb - 1)]++;
+    pt->entries[2 * e] = keys[i];
+    pt->entries[2 * e + 1] = static_cast<uint32_t>(i);
+  }
+}
+
+uint64_t filter_reads(const Plan& P, uint64_t n) {
+  const ScanPlan& sp = P.sp;
+  if (sp.overlapping) return n >= sp.q ? n - sp.q + 1 : 0;
+  return (n / sp.q) / sp.k;
+}
+
+void sample_offsets(size_t corpus_len, size_t count, size_t length, uint64_t seed,
+                    std::vector<uint64_t>* out) {
+  uint64_t s = seed;
+  const uint64_t span = corpus_len - length + 1;
+  out->resize(count);
+  for (size_t i = 0; i < count; ++i) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    (*out)[i] = z % span;
+  }
+}
+
+}  // namespace magb

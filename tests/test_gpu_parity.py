@@ -1,0 +1,214 @@
+"""GPU parity: the sm_100a search path (through the C ABI) against the
+reference's own compiled oracles and the C restatement.
+
+Bar: bit-exact (offset, pattern_index) sets; identical filter counters
+(reads, candidates) to the restated reference machine at identical
+(variant, q, k, sigma', map, w, gram mode).
+"""
+import numpy as np
+import pytest
+
+from pyoracle import as_pairs
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_pairs(engine, text):
+    m = engine.search(text)
+    return m.pairs(), m.metrics()
+
+
+def rand_instance(rng, sig=None, n=None, r=None, m=None, unequal=True, copy_frac=0.5, base=97):
+    sig = sig or int(rng.choice([2, 4, 16, 64, 200]))
+    n = int(rng.integers(0, 20000)) if n is None else n
+    r = r or int(rng.integers(1, 40))
+    m = m or int(rng.integers(1, 40))
+    text = (rng.integers(0, sig, n) + base).astype(np.uint8)
+    pats = []
+    for _ in range(r):
+        L = m + (int(rng.integers(0, 5)) if unequal else 0)
+        if n > L and rng.random() < copy_frac:
+            s = int(rng.integers(0, n - L + 1))
+            pats.append(text[s:s + L].tobytes())
+        else:
+            pats.append((rng.integers(0, sig, L) + base).astype(np.uint8).tobytes())
+    return text, pats
+
+
+def test_spec_examples(mag, ref):
+    # SPEC.md:55-57, 65-66, 382, 516 (results as (offset, pattern_index))
+    cases = [
+        (b"xabbacy", [b"abba", b"bbac"], [(1, 0), (2, 1)]),
+        (b"aaa", [b"aa"], [(0, 0), (1, 0)]),
+        (b"abab", [b"zz"], []),
+        (b"ushers", [b"he", b"she", b"his"], [(1, 1), (2, 0)]),
+        (b"", [b"ab"], []),
+        (b"zabbaz", [b"abba"], [(1, 0)]),
+    ]
+    for text, pats, want in cases:
+        assert as_pairs(*ref.naive(text, pats)) == want
+        for variant in ("mag", "smag", "shiftor_og"):
+            e = mag.Engine(pats, variant=variant)
+            got, _ = gpu_pairs(e, text)
+            assert got == want, (text, pats, variant, e.plan())
+        # the reference's own parameter path (exact grams, q = 1)
+        e = mag.Engine(pats, q=1, k=1, mapping="identity")
+        assert gpu_pairs(e, text)[0] == want
+
+
+def test_random_auto_plans(mag, ref):
+    rng = np.random.default_rng(11)
+    for it in range(120):
+        text, pats = rand_instance(rng)
+        want = as_pairs(*ref.ac(text, pats))
+        variant = ["mag", "smag", "shiftor_og"][it % 3]
+        e = mag.Engine(pats, variant=variant)
+        got, met = gpu_pairs(e, text)
+        assert got == want, (it, variant, e.plan())
+
+
+@pytest.mark.parametrize("mapping", ["identity", "freq", "balance", "lowbits"])
+def test_reference_parameters_and_counters(mag, ref, port, mapping):
+    """Exact-gram plans with explicit (q, k, sigma', map): same matches as the
+    reference oracles, same filter reads/candidates as the restated machine."""
+    rng = np.random.default_rng(hash(mapping) & 0xffff)
+    for it in range(40):
+        sig = int(rng.choice([2, 4, 16, 64]))
+        text, pats = rand_instance(rng, sig=sig, m=int(rng.integers(2, 33)))
+        mm = min(len(p) for p in pats)
+        variant = ["mag", "smag", "shiftor_og"][it % 3]
+        if variant == "shiftor_og":
+            qmax = min(8, mm)
+        else:
+            qmax = min(8, (mm + 1) // 2)
+        q = int(rng.integers(1, qmax + 1))
+        kk = 0 if variant == "shiftor_og" else int(rng.integers(1, (mm - q + 1) // q + 1))
+        kw = dict(variant=variant, q=q, k=kk, mapping=mapping)
+        if mapping == "lowbits":
+            kw["lowbits"] = int(rng.integers(1, 9))
+            if (1 << kw["lowbits"]) ** q > (1 << 24):
+                continue
+        elif mapping in ("freq", "balance"):
+            kw["sigma_prime"] = int(rng.integers(2, 17))
+            if kw["sigma_prime"] ** q > (1 << 24):
+                continue
+        elif 256 ** q > (1 << 24):
+            continue
+        e = mag.Engine(pats, **kw)
+        got, met = gpu_pairs(e, text)
+        want = as_pairs(*ref.ac(text, pats))
+        assert got == want, (it, kw)
+        info = e.info()
+        table, sp = e.alphabet()
+        P = port.params(variant={"mag": 0, "smag": 1, "shiftor_og": 2}[variant], gram_mode=0, q=info.q,
+                        k=info.k, sigma_prime=sp, table=table)
+        o, p, reads, cands = port.search(text, pats, P)
+        assert as_pairs(o, p) == want
+        assert (met.filter_reads, met.candidates) == (reads, cands), (it, kw)
+
+
+def test_hashed_counters_match_port(mag, ref, port):
+    rng = np.random.default_rng(5)
+    for it in range(40):
+        text, pats = rand_instance(rng, sig=4, n=int(rng.integers(1000, 60000)), r=int(rng.integers(1, 300)),
+                                   m=int(rng.integers(4, 40)), base=65)
+        variant = ["mag", "shiftor_og"][it % 2]
+        e = mag.Engine(pats, variant=variant)
+        pl = e.plan()
+        got, met = gpu_pairs(e, text)
+        assert got == as_pairs(*ref.ac(text, pats))
+        if pl["verify_all"]:
+            assert met.candidates == met.filter_reads
+            continue
+        P = port.params(variant=0 if variant == "mag" else 2, gram_mode=1, q=pl["q"], k=pl["k"],
+                        table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"])
+        o, p, reads, cands = port.search(text, pats, P)
+        assert (met.filter_reads, met.candidates) == (reads, cands), (it, pl)
+
+
+def test_edge_cases(mag, ref):
+    cases = []
+    cases.append((b"", [b"a"]))                       # empty text
+    cases.append((b"abc", [b"abcd"]))                 # n < m
+    cases.append((b"ab", [b"abcdefgh"]))              # n < q for most plans
+    cases.append((b"abcabc", [b"abc", b"abc", b"bc"]))  # duplicates keep both ids
+    cases.append((b"xyzxyz", [b"xyz", b"yzxyz"]))     # match at 0 and at n-m
+    cases.append((b"a" * 5000, [b"a", b"aa", b"aaa"]))  # every position, every pattern
+    cases.append((b"a" * 70000, [b"aaaa"] * 7))       # dense + duplicates: output overflow path
+    for text, pats in cases:
+        want = as_pairs(*ref.naive(text, pats))
+        for variant in ("mag", "smag", "shiftor_og"):
+            e = mag.Engine(pats, variant=variant)
+            assert gpu_pairs(e, text)[0] == want, (text[:20], pats, variant)
+
+
+def test_tile_boundaries(mag, ref):
+    """Texts whose occurrences straddle tile and warp-slice boundaries."""
+    rng = np.random.default_rng(7)
+    for tile in (256, 1024, 8192):
+        for it in range(6):
+            n = tile * int(rng.integers(1, 6)) + int(rng.integers(-40, 40))
+            text, pats = rand_instance(rng, sig=4, n=max(n, 0), r=20, m=int(rng.integers(5, 30)), base=65)
+            # plant occurrences right around every tile boundary
+            text = text.copy()
+            for b in range(tile, text.size, tile):
+                p = pats[int(rng.integers(0, len(pats)))]
+                s = max(0, b - int(rng.integers(0, len(p))))
+                if s + len(p) <= text.size:
+                    text[s:s + len(p)] = np.frombuffer(p, dtype=np.uint8)
+            want = as_pairs(*ref.ac(text, pats))
+            for variant in ("mag", "shiftor_og"):
+                e = mag.Engine(pats, variant=variant, tile_bytes=tile, warps=int(rng.choice([1, 4, 16])))
+                assert gpu_pairs(e, text)[0] == want, (tile, it, variant, e.plan())
+
+
+def test_long_patterns_beyond_halo(mag, ref):
+    rng = np.random.default_rng(9)
+    text = (rng.integers(0, 4, 50000) + 65).astype(np.uint8)
+    pats = [text[s:s + L].tobytes() for s, L in ((100, 2000), (9000, 1500), (30000, 3000), (49000, 1000))]
+    pats.append(text[8000:8050].tobytes())
+    want = as_pairs(*ref.ac(text, pats))
+    for variant in ("mag", "shiftor_og"):
+        assert gpu_pairs(mag.Engine(pats, variant=variant), text)[0] == want
+
+
+def test_prepared_async_and_device_text(mag, ref):
+    import torch
+    rng = np.random.default_rng(3)
+    text, pats = rand_instance(rng, sig=4, n=300000, r=50, m=20, base=65)
+    want = as_pairs(*ref.ac(text, pats))
+    e = mag.Engine(pats)
+    p = e.prepare(text)
+    assert e.search_prepared(p).pairs() == want
+    d = torch.from_numpy(text).cuda()
+    pd = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
+    s = torch.cuda.Stream()
+    ms = [e.search_prepared_async(pd, s.cuda_stream) for _ in range(3)]
+    for m in ms:
+        assert m.pairs() == want
+    # misaligned device pointer -> internal aligned copy
+    pd2 = e.prepare_device(d.data_ptr() + 3, d.numel() - 3, keep=d)
+    want2 = as_pairs(*ref.ac(text[3:], pats))
+    assert e.search_prepared(pd2).pairs() == want2
+
+
+def test_smag_codes_equal_reference_encode_text(mag, ref):
+    rng = np.random.default_rng(4)
+    text, pats = rand_instance(rng, sig=4, n=10000, r=10, m=16, base=65)
+    for q in (1, 3, 5, 8):
+        e = mag.Engine(pats, variant="smag", q=q, k=1, mapping="balance", sigma_prime=4)
+        p = e.prepare(text)
+        want = ref.encode_text(2, pats, 4, 0, q, text)
+        assert np.array_equal(p.codes(text.size // q), want)
+
+
+@pytest.mark.parametrize("cfg,scale", [(1, 1.0), (2, 1 / 64), (3, 1 / 32), (4, 1 / 64), (5, 1 / 64)])
+def test_baseline_configs_reduced(mag, ref, cfg, scale):
+    from paper_1405_5483_b200 import workloads
+    w = workloads.generate(cfg, scale)
+    want = ref.ac(w.text, w.patterns, threads=8)
+    e = mag.Engine(w.patterns)
+    m = e.search(w.text)
+    offs, pids = m.arrays()
+    assert np.array_equal(offs, want[0]) and np.array_equal(pids, want[1]), (cfg, e.plan())
+    assert m.metrics().filter_reads == (w.text.size // e.info().q) // e.info().k or e.plan()["verify_all"]
