@@ -55,21 +55,27 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // Per-search device scratch, pooled per engine.  `done` orders reuse on the
 // device (a later search waits for it with cudaStreamWaitEvent).
 struct Workspace {
-  unsigned long long* ctrl = nullptr;  // status[num_tiles] | counters[4] | tickets[kMaxLaunch]
-  size_t ctrl_cap = 0;                 // in words
-  uint64_t* out = nullptr;
+  unsigned long long* ctrl = nullptr;  // counters[8] | tickets[kMaxLaunch]
+  uint32_t* counts = nullptr;          // per-slice match counts
+  size_t counts_cap = 0;
+  uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
+  uint64_t* out = nullptr;             // sorted matches (same capacity)
   size_t out_cap = 0;
-  unsigned long long* h_ctr = nullptr;  // pinned copy of counters[4]
+  unsigned long long* h_ctr = nullptr;  // pinned copy of counters[8]
   uint8_t* text = nullptr;              // device copy of host text (mag_search)
   size_t text_cap = 0;
   cudaStream_t copy_stream = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   cudaEvent_t done = nullptr;
   int device = 0;
+  // geometry of the last enqueued search
+  uint64_t num_slices = 0, slice_cap = 0;
 
   ~Workspace() {
     cudaSetDevice(device);
     if (ctrl) cudaFree(ctrl);
+    if (counts) cudaFree(counts);
+    if (staging) cudaFree(staging);
     if (out) cudaFree(out);
     if (h_ctr) cudaFreeHost(h_ctr);
     if (text) cudaFree(text);
@@ -133,6 +139,8 @@ struct mag_engine {
   uint64_t* d_pat_off = nullptr;
   uint32_t* d_pat_len = nullptr;
   uint8_t* d_map = nullptr;
+  // learned output density: max matches per slice seen so far, per sample
+  mutable double slice_density = 0;
   // pool
   mutable std::mutex mu;
   mutable std::vector<std::unique_ptr<Workspace>> pool;
@@ -209,43 +217,77 @@ void release(const mag_engine* e, std::unique_ptr<Workspace> w) {
   e->pool.push_back(std::move(w));
 }
 
-mag_status ensure_ws(Workspace* w, size_t ctrl_words, size_t out_cap) {
-  if (!w->done) MAG_CUDA(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
-  if (!w->h_ctr) MAG_CUDA(cudaMallocHost(&w->h_ctr, 4 * sizeof(unsigned long long)));
-  if (w->ctrl_cap < ctrl_words) {
-    if (w->ctrl) MAG_CUDA(cudaFree(w->ctrl));
-    w->ctrl = nullptr;
-    MAG_CUDA(cudaMalloc(&w->ctrl, ctrl_words * sizeof(unsigned long long)));
-    w->ctrl_cap = ctrl_words;
+constexpr size_t kCounters = 8;
+
+struct SearchGeometry {
+  uint64_t samples, num_slices, slice_cap;
+};
+
+SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) {
+  const Plan& P = e->plan;
+  SearchGeometry g;
+  g.samples = filter_reads(P, n);
+  g.num_slices = (g.samples + P.slice_samples - 1) / P.slice_samples;
+  if (cap_override) {
+    g.slice_cap = cap_override;
+  } else {
+    double dens;
+    {
+      std::lock_guard<std::mutex> lk(e->mu);
+      dens = e->slice_density;
+    }
+    // until a search has been seen: 1 match per 128 text bytes of a slice
+    const double bytes = static_cast<double>(P.slice_samples) *
+                         (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
+    const double guess = std::max(dens * static_cast<double>(P.slice_samples) * 1.25, bytes / 128);
+    g.slice_cap = std::max<uint64_t>(64, static_cast<uint64_t>(guess) + 32);
   }
-  if (w->out_cap < out_cap) {
+  return g;
+}
+
+mag_status ensure_ws(Workspace* w, const SearchGeometry& g) {
+  if (!w->done) MAG_CUDA(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
+  if (!w->h_ctr) MAG_CUDA(cudaMallocHost(&w->h_ctr, kCounters * sizeof(unsigned long long)));
+  if (!w->ctrl) MAG_CUDA(cudaMalloc(&w->ctrl, (kCounters + kMaxLaunch) * sizeof(unsigned long long)));
+  if (w->counts_cap < std::max<uint64_t>(1, g.num_slices)) {
+    if (w->counts) MAG_CUDA(cudaFree(w->counts));
+    w->counts = nullptr;
+    w->counts_cap = std::max<uint64_t>(1, g.num_slices);
+    MAG_CUDA(cudaMalloc(&w->counts, w->counts_cap * sizeof(uint32_t)));
+  }
+  const size_t cap = std::max<size_t>(1, g.num_slices * g.slice_cap);
+  if (w->out_cap < cap) {
     if (w->out) MAG_CUDA(cudaFree(w->out));
-    w->out = nullptr;
-    MAG_CUDA(cudaMalloc(&w->out, out_cap * sizeof(uint64_t)));
-    w->out_cap = out_cap;
+    if (w->staging) MAG_CUDA(cudaFree(w->staging));
+    w->out = w->staging = nullptr;
+    w->out_cap = 0;
+    MAG_CUDA(cudaMalloc(&w->staging, cap * sizeof(uint64_t)));
+    MAG_CUDA(cudaMalloc(&w->out, cap * sizeof(uint64_t)));
+    w->out_cap = cap;
   }
   return MAG_OK;
 }
 
-struct TileRange {
+struct SliceRange {
   uint64_t begin, end;
   cudaEvent_t wait;  // may be null
 };
 
-// Enqueue one complete search over device text: zero the look-back state,
-// run the fused kernel over the tile ranges, copy the counters back (pinned),
-// record ws->done.  All on `st`.
+// Enqueue one complete search over device text: zero the control words, run
+// the fused kernel over the slice ranges, gather the staged slices, copy the
+// counters back (pinned), record ws->done.  All on `st`.
 mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_text, uint64_t n,
                           const uint32_t* d_codes, cudaStream_t st,
-                          const std::vector<TileRange>& ranges) {
+                          const std::vector<SliceRange>& ranges, uint64_t cap_override = 0) {
   const Plan& P = e->plan;
-  const uint64_t num_tiles = n ? (n + P.tile_bytes - 1) / P.tile_bytes : 0;
-  const size_t ctrl_words = num_tiles + 4 + kMaxLaunch;
-  size_t want_out = w->out_cap ? w->out_cap : std::max<size_t>(1 << 16, n / 64);
-  mag_status s = ensure_ws(w, ctrl_words, want_out);
+  const SearchGeometry g = geometry(e, n, cap_override);
+  mag_status s = ensure_ws(w, g);
   if (s != MAG_OK) return s;
-  MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, ctrl_words * sizeof(unsigned long long), st));
-  if (num_tiles) {
+  w->num_slices = g.num_slices;
+  w->slice_cap = g.slice_cap;
+  MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, (kCounters + kMaxLaunch) * sizeof(unsigned long long), st));
+  unsigned long long* counters = w->ctrl;
+  if (g.num_slices) {
     ScanArgs a{};
     a.plan = P.sp;
     a.text = d_text;
@@ -259,34 +301,35 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.pat_off = e->d_pat_off;
     a.pat_len = e->d_pat_len;
     a.map = e->d_map;
-    a.samples = filter_reads(P, n);
-    a.tile_bytes = P.tile_bytes;
-    a.num_tiles = num_tiles;
-    a.halo = P.halo;
+    a.samples = g.samples;
+    a.slice_samples = P.slice_samples;
+    a.chunk_samples = P.chunk_samples;
+    a.back = P.back;
+    a.slot_bytes = P.slot_bytes;
+    a.ring = P.ring;
     a.nwarps = P.nwarps;
-    a.stages = P.stages;
-    a.mbuf = P.mbuf;
-    a.out = w->out;
-    a.out_cap = w->out_cap;
-    a.status = w->ctrl;
-    a.counters = w->ctrl + num_tiles;
+    a.num_slices = g.num_slices;
+    a.staging = w->staging;
+    a.slice_cap = static_cast<uint32_t>(std::min<uint64_t>(g.slice_cap, 0xffffffffu));
+    a.slice_count = w->counts;
+    a.counters = counters;
     size_t li = 0;
-    for (const TileRange& r : ranges) {
+    for (const SliceRange& r : ranges) {
       if (r.wait) MAG_CUDA(cudaStreamWaitEvent(st, r.wait, 0));
       if (r.end <= r.begin) continue;
-      a.tile_begin = r.begin;
-      a.tile_end = r.end;
-      a.ticket = w->ctrl + num_tiles + 4 + (li++ % kMaxLaunch);
-      const uint64_t tiles = r.end - r.begin;
-      const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(e->sm_count)));
+      a.slice_begin = r.begin;
+      a.slice_end = r.end;
+      a.ticket = counters + kCounters + (li++ % kMaxLaunch);
+      const uint64_t ctas = (r.end - r.begin + P.nwarps - 1) / P.nwarps;
+      const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
       MAG_CUDA(timed_launch(a, st, grid));
     }
-    MAG_CUDA(cudaMemcpyAsync(w->h_ctr, a.counters, 4 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st));
-  } else {
-    MAG_CUDA(cudaMemcpyAsync(w->h_ctr, w->ctrl, 4 * sizeof(unsigned long long),
-                             cudaMemcpyDeviceToHost, st));
+    const int cgrid = static_cast<int>(std::min<uint64_t>(
+        std::max<uint64_t>(1, g.num_slices / 8), static_cast<uint64_t>(e->sm_count)));
+    MAG_CUDA(launch_compact(a, w->out, w->out_cap, st, cgrid));
   }
+  MAG_CUDA(cudaMemcpyAsync(w->h_ctr, counters, kCounters * sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, st));
   MAG_CUDA(cudaEventRecord(w->done, st));
   return MAG_OK;
 }
@@ -296,28 +339,28 @@ uint64_t analytic_candidates(const Plan& P, uint64_t n) {
   return filter_reads(P, n);
 }
 
-// Waits for a pending search, reruns it if the output capacity overflowed,
-// copies the sorted keys to the host.
+// Waits for a pending search, reruns it if a slice overflowed its staging
+// capacity (counts are exact even then), copies the sorted keys to the host.
 mag_status materialize(mag_matches* m) {
   if (!m->pending) return m->sticky;
   const mag_engine* e = m->engine;
   cudaSetDevice(e->device);
   Workspace* w = m->ws.get();
   MAG_CUDA(cudaEventSynchronize(w->done));
-  unsigned long long total = w->h_ctr[2];
-  if (total > w->out_cap) {
-    // Grow to the exact size and run again (same stream, same inputs).
-    if (w->out) MAG_CUDA(cudaFree(w->out));
-    w->out = nullptr;
-    w->out_cap = 0;
-    MAG_CUDA(cudaMalloc(&w->out, total * sizeof(uint64_t)));
-    w->out_cap = total;
-    const uint64_t num_tiles = (m->n + e->plan.tile_bytes - 1) / e->plan.tile_bytes;
+  unsigned long long total = w->h_ctr[2], maxc = w->h_ctr[3];
+  if (maxc > w->slice_cap) {
+    const uint64_t slices = w->num_slices;
     mag_status s = enqueue_search(e, w, m->d_text, m->n, m->d_codes, m->stream,
-                                  {TileRange{0, num_tiles, nullptr}});
+                                  {SliceRange{0, slices, nullptr}}, maxc);
     if (s != MAG_OK) return s;
     MAG_CUDA(cudaEventSynchronize(w->done));
     total = w->h_ctr[2];
+    maxc = w->h_ctr[3];
+  }
+  {
+    const double dens = static_cast<double>(maxc) / static_cast<double>(e->plan.slice_samples);
+    std::lock_guard<std::mutex> lk(e->mu);
+    e->slice_density = std::max(e->slice_density, dens);
   }
   m->keys.resize(total);
   if (total)
@@ -535,11 +578,12 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->key_len = P.sp.key_len;
   out->prefilter_bits = P.sp.pf_bits;
   out->bucket_bits = P.sp.bucket_bits;
-  out->tile_bytes = P.tile_bytes;
-  out->halo = P.halo;
+  out->tile_bytes = static_cast<uint32_t>(
+      P.chunk_samples * (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k));
+  out->halo = P.back;
   out->warps = P.nwarps;
-  out->stages = P.stages;
-  out->smem_bytes = smem_layout(P.sp, P.tile_bytes, P.halo, P.stages, P.nwarps, P.mbuf).total;
+  out->stages = P.ring;
+  out->smem_bytes = plan_smem(P);
   out->predicted_candidates_per_byte = P.pred_cand_per_byte;
   return MAG_OK;
 }
@@ -633,9 +677,9 @@ MAG_API mag_status mag_search_prepared_async(const mag_engine* e, const mag_prep
     m->d_codes = p->d_codes;
     m->n = p->len;
     if (m->ws->done) MAG_CUDA(cudaStreamWaitEvent(m->stream, m->ws->done, 0));
-    const uint64_t num_tiles = p->len ? (p->len + e->plan.tile_bytes - 1) / e->plan.tile_bytes : 0;
+    const uint64_t slices = geometry(e, p->len, 1).num_slices;
     s = enqueue_search(e, m->ws.get(), p->d_text, p->len, p->d_codes, m->stream,
-                       {TileRange{0, num_tiles, nullptr}});
+                       {SliceRange{0, slices, nullptr}});
     if (s != MAG_OK) return s;
     m->pending = true;
     *out = m.release();
@@ -697,11 +741,12 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
     // the copy stream must not overwrite text a previous search still reads
     if (w->done) MAG_CUDA(cudaStreamWaitEvent(w->copy_stream, w->done, 0));
     const Plan& P = e->plan;
-    const uint64_t tile = P.tile_bytes;
-    const uint64_t num_tiles = len ? (len + tile - 1) / tile : 0;
+    const uint64_t slices = geometry(e, len, 1).num_slices;
+    const uint64_t slice_bytes =
+        P.slice_samples * (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
     const uint64_t chunk = std::max<uint64_t>(uint64_t(64) << 20, (len + 31) / 32);
-    std::vector<TileRange> ranges;
-    uint64_t copied = 0, tiles_done = 0;
+    std::vector<SliceRange> ranges;
+    uint64_t copied = 0, slices_done = 0;
     size_t ci = 0;
     while (copied < len) {
       const uint64_t nb = std::min<uint64_t>(chunk, len - copied);
@@ -714,12 +759,12 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
         w->chunk_ev.push_back(ev);
       }
       MAG_CUDA(cudaEventRecord(w->chunk_ev[ci], w->copy_stream));
-      // tiles whose staged window [A0, A0+tile+halo) is fully copied
-      uint64_t ready = copied == len ? num_tiles
-                                     : (copied > P.halo ? (copied - P.halo) / tile : 0);
-      ready = std::min(ready, num_tiles);
-      ranges.push_back(TileRange{tiles_done, ready, w->chunk_ev[ci]});
-      tiles_done = ready;
+      // slices whose bytes (plus the pattern reach) have fully arrived
+      const uint64_t reach = P.back + 64;
+      uint64_t ready = copied == len ? slices : (copied > reach ? (copied - reach) / slice_bytes : 0);
+      ready = std::min(ready, slices);
+      ranges.push_back(SliceRange{slices_done, ready, w->chunk_ev[ci]});
+      slices_done = std::max(slices_done, ready);
       ++ci;
     }
     m->d_text = w->text;

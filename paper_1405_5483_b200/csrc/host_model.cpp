@@ -203,10 +203,10 @@ bool tune(const TuningInput& in, int fixed_q, int fixed_k, TuningResult* out, st
 // ------------------------------------------------------------------ plan
 namespace {
 
-constexpr uint32_t kDefaultTile = 8192;
-constexpr uint32_t kDefaultStages = 4;
+constexpr uint32_t kChunkTarget = 1024;   // gram bytes per ring slot
+constexpr uint32_t kSliceTarget = 32768;  // text bytes per warp work item
+constexpr uint32_t kDefaultRing = 3;
 constexpr uint32_t kDefaultWarps = 16;
-constexpr uint32_t kMbuf = 32;
 
 unsigned pow2ceil_log2(unsigned x) {
   unsigned l = 0;
@@ -243,35 +243,38 @@ double prefilter_fp(double keys, unsigned pf_bits) {
 constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 12,
                  kCostProbe = 150, kCostVerifyAll = 16;
 
-uint32_t gcd32(uint32_t a, uint32_t b) {
-  while (b) {
-    uint32_t t = a % b;
-    a = b;
-    b = t;
-  }
-  return a;
-}
-
+// Chunk / slice / slot sizes of the warp-streaming kernel.
 void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
-  ScanPlan& sp = P->sp;
-  const uint32_t gs = sp.overlapping ? 1 : sp.q;
-  const uint32_t step = 16 / gcd32(16, gs) * gs;  // lcm(16, gram step)
-  uint32_t tile = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes) : kDefaultTile;
-  tile = std::max(step, tile / step * step);
-  P->tile_bytes = tile;
-  const uint64_t reach = sp.verify_all ? 16 : static_cast<uint64_t>(gs) * sp.k * sp.m_prime + sp.q;
-  const uint64_t verify_reach = std::min<uint64_t>(pd.maxlen, 1024);
-  P->halo = static_cast<uint32_t>(align16(std::max<uint64_t>(reach, verify_reach) + 32));
-  P->stages = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultStages;
+  const ScanPlan& sp = P->sp;
+  const uint32_t ov = sp.m_prime ? sp.m_prime - 1 : 0;
+  const uint32_t adv = sp.verify_all ? 32 : (sp.m_prime <= 16 ? 32 - ov : 32);
+  const uint32_t bytes_per_sample = sp.verify_all || sp.overlapping ? 1 : sp.q * sp.k;
+  const uint32_t target = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes) : kChunkTarget;
+  const uint32_t iters = std::max<uint32_t>(1, (target + adv * bytes_per_sample / 2) / (adv * bytes_per_sample));
+  P->chunk_samples = iters * adv;
+  const uint64_t chunk_bytes = static_cast<uint64_t>(P->chunk_samples) * bytes_per_sample;
+  P->slice_samples = static_cast<uint64_t>(P->chunk_samples) *
+                     std::max<uint64_t>(1, (kSliceTarget + chunk_bytes / 2) / chunk_bytes);
+  // pattern reach after the last gram: full patterns up to 1 KiB stay in the
+  // slot, longer ones are compared from global memory; >= 16 + 4 key bytes
+  P->back = static_cast<uint32_t>(std::min<uint64_t>(pd.maxlen, 1024) + 24);
+  uint64_t window;
+  if (sp.verify_all)
+    window = P->chunk_samples;
+  else if (sp.overlapping)
+    window = static_cast<uint64_t>(P->chunk_samples) + ov + sp.q;
+  else
+    window = (static_cast<uint64_t>(P->chunk_samples) + ov) * sp.q * sp.k + sp.q;
+  P->slot_bytes = static_cast<uint32_t>(align16(window + P->back + 15 + 32));
+  P->ring = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultRing;
   P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kDefaultWarps;
-  P->mbuf = kMbuf;
 }
 
 size_t fixed_smem(const Plan& P) {
   ScanPlan z = P.sp;
   z.table_in_smem = 0;
   z.pf_bits = 0;
-  return smem_layout(z, P.tile_bytes, P.halo, P.stages, P.nwarps, P.mbuf).total;
+  return smem_layout(z, P.slot_bytes, P.ring, P.nwarps).total;
 }
 
 void set_entry_geometry(ScanPlan& sp) {
@@ -310,11 +313,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   sp.maxlen = static_cast<uint32_t>(std::min<size_t>(pd.maxlen, 0xffffffffu));
   sp.r = static_cast<uint32_t>(pd.r);
   sp.key_len = static_cast<uint32_t>(std::min<size_t>(pd.m, 16));
-  {
-    uint32_t pw = 1;
-    for (uint32_t i = 1; i < sp.key_len; ++i) pw *= kKeyBase;
-    sp.key_pow = pw;
-  }
   const uint32_t sigma_obs = std::max(1u, h.distinct());
   const size_t m = pd.m;
   const unsigned w = rq.word_bits > 0 ? std::min(64, rq.word_bits) : 64;
@@ -378,14 +376,17 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->mapping = kMapIdentity;
     for (int c = 0; c < 256; ++c) P->map[c] = static_cast<uint8_t>(c);
     sp.sigma_prime = 256;
-    Plan probe = *P;
-    probe.sp.q = 1;
-    probe.sp.k = 1;
-    probe.sp.m_prime = 1;
-    finish_geometry(pd, rq, &probe);
-    const size_t room = rq.smem_limit > fixed_smem(probe) + 4096
-                            ? rq.smem_limit - fixed_smem(probe) - 4096
-                            : 0;
+    // shared memory left for table + prefilter once the warp rings are in
+    auto room_for = [&](unsigned q, unsigned k, unsigned mp, int va) {
+      Plan probe = *P;
+      probe.sp.q = q;
+      probe.sp.k = k;
+      probe.sp.m_prime = mp;
+      probe.sp.verify_all = va;
+      finish_geometry(pd, rq, &probe);
+      const size_t f = fixed_smem(probe) + 1024;
+      return rq.smem_limit > f ? rq.smem_limit - f : size_t(0);
+    };
     const double keys = static_cast<double>(pd.r);
     struct Cand {
       double cost = std::numeric_limits<double>::infinity();
@@ -395,6 +396,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     } best;
     // verify-all baseline: whole room to the prefilter
     {
+      const size_t room = room_for(1, 1, 1, 1);
       unsigned pf = 7;
       while (pf < 24 && (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
       best.cost = kCostVerifyAll + prefilter_fp(keys, pf) * kCostProbe;
@@ -414,6 +416,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           if (rq.k > 0 && !sp.overlapping && k != static_cast<unsigned>(rq.k)) continue;
           const unsigned mpmax = static_cast<unsigned>(std::min<size_t>(L / k, w / k));
           for (unsigned mp = 1; mp <= mpmax; ++mp) {
+            const size_t room = room_for(q, k, mp, 0);
             const unsigned el = pow2ceil_log2(std::max(1u, k * mp));
             for (unsigned tbits = 14; tbits <= 24; ++tbits) {
               const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
@@ -515,13 +518,19 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     while ((size_t(1) << bb) < 2 * pd.r && bb < 26) ++bb;
     sp.bucket_bits = bb;
   }
-  const size_t total = smem_layout(sp, P->tile_bytes, P->halo, P->stages, P->nwarps, P->mbuf).total;
+  // oversized rings (long patterns, wide windows): fewer warps per CTA
+  while (plan_smem(*P) > rq.smem_limit && P->nwarps > 1) P->nwarps /= 2;
+  const size_t total = plan_smem(*P);
   if (total > rq.smem_limit) {
     *err = "plan needs " + std::to_string(total) + " bytes of shared memory (limit " +
            std::to_string(rq.smem_limit) + ")";
     return kBadConfig;
   }
   return kOk;
+}
+
+size_t plan_smem(const Plan& p) {
+  return smem_layout(p.sp, p.slot_bytes, p.ring, p.nwarps).total;
 }
 
 // --------------------------------------------------------------- tables
@@ -591,7 +600,7 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   const ScanPlan& sp = P.sp;
   const size_t r = pd.r;
   std::vector<uint32_t> keys(r);
-  for (size_t i = 0; i < r; ++i) keys[i] = key_mix(key_poly(pd.pattern(i), sp.key_len));
+  for (size_t i = 0; i < r; ++i) keys[i] = key_bytes(pd.pattern(i), sp.key_len);
   // prefilter: two probes per key (scan_kernels.cu prefilter_pass)
   const size_t pf_words = std::max<size_t>(4, (size_t(1) << sp.pf_bits) / 32);
   pt->prefilter.assign(align16(pf_words * 4) / 4, 0);

@@ -72,7 +72,7 @@ struct PlanRequest {
   int gram_mode = -1;        // mag_gram_mode
   int table_bits = 0;        // hashed: 0 auto, -1 verify-all
   int word_bits = 0;
-  int tile_bytes = 0, warps = 0, stages = 0;
+  int tile_bytes = 0, warps = 0, stages = 0;  // tile_bytes: chunk bytes target; stages: ring
   size_t smem_limit = 232448;  // sm_100 max dynamic shared memory per CTA
 };
 
@@ -81,9 +81,16 @@ struct Plan {
   int variant = 0;
   int mapping = 0;           // mag_mapping in effect
   uint8_t map[256] = {0};
-  uint32_t tile_bytes = 0, halo = 0, nwarps = 0, stages = 0, mbuf = 0;
+  // kernel geometry (scan_launch.h ScanArgs)
+  uint32_t chunk_samples = 0;  // samples per ring slot
+  uint64_t slice_samples = 0;  // samples per warp work item
+  uint32_t back = 0;           // staged bytes after a chunk's last gram
+  uint32_t slot_bytes = 0;
+  uint32_t ring = 0, nwarps = 0;
   double pred_cand_per_byte = 0;
 };
+
+size_t plan_smem(const Plan& p);
 
 // Errors: returns a mag_status value (0 ok) and fills *err.
 int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, Plan* plan,

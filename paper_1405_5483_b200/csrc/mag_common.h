@@ -56,11 +56,9 @@ MAG_HD uint32_t gram_slot(uint32_t h, unsigned table_bits) {
   return table_bits ? (h >> (32 - table_bits)) : 0u;
 }
 
-// Verification key: polynomial hash of the first v bytes (v = min(m, 16)),
-// H = sum b[i] * B^(v-1-i) mod 2^32, then a murmur3 finaliser.  Polynomial so
-// the device can roll it across consecutive starts.
-constexpr uint32_t kKeyBase = 0x01000193u;
-
+// Verification key: the first v = min(m, 16) bytes of a start, read as four
+// little-endian words (bytes past v zeroed), mixed.  Top bits index the
+// shared-memory prefilter, low bits the bucket table.
 MAG_HD uint32_t key_mix(uint32_t h) {
   h ^= h >> 16;
   h *= 0x85EBCA6Bu;
@@ -70,10 +68,21 @@ MAG_HD uint32_t key_mix(uint32_t h) {
   return h;
 }
 
-MAG_HD uint32_t key_poly(const uint8_t* p, unsigned v) {
-  uint32_t h = 0;
-  for (unsigned i = 0; i < v; ++i) h = h * kKeyBase + p[i];
-  return h;
+MAG_HD uint32_t key_words(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3) {
+  return key_mix(x0 * 0x9E3779B1u + x1 * 0x7FEB352Du + x2 * 0x846CA68Bu + x3 * 0x68E31DA4u);
+}
+
+MAG_HD uint32_t key_bytes(const uint8_t* p, unsigned v) {
+  uint32_t x[4] = {0, 0, 0, 0};
+  for (unsigned i = 0; i < v; ++i) x[i >> 2] |= (uint32_t)p[i] << (8 * (i & 3));
+  return key_words(x[0], x[1], x[2], x[3]);
+}
+
+// Byte masks of the v-byte key per word.
+MAG_HD uint32_t key_word_mask(unsigned v, unsigned word) {
+  if (v >= 4 * (word + 1)) return 0xffffffffu;
+  if (v <= 4 * word) return 0u;
+  return (1u << (8 * (v - 4 * word))) - 1u;
 }
 
 // Scan plan shared by host and kernels (passed by value to the kernel).
@@ -93,7 +102,6 @@ struct ScanPlan {
   uint64_t match_mask;
   // verification
   uint32_t m, maxlen, key_len;
-  uint32_t key_pow;       // kKeyBase^(key_len-1) mod 2^32, for rolling
   uint32_t pf_bits;       // prefilter bitmap has 2^pf_bits bits (smem)
   uint32_t bucket_bits;   // 2^bucket_bits buckets (global)
   uint32_t r;
@@ -102,28 +110,26 @@ struct ScanPlan {
 
 // ---- shared-memory layout of the scan kernel (host computes the size,
 // device carves it; one definition for both).
-constexpr int kMaxWarps = 16;   // consumer warps per CTA
+constexpr int kMaxWarps = 16;   // warps per CTA (launch bound: 512 threads)
 constexpr int kQueueCap = 64;   // candidate windows queued per warp
 
-struct StageMeta {
-  long long tile;               // -1: end of work
-  unsigned long long excl;      // exclusive prefix of the tile (if excl_ready)
-  unsigned int done;            // consumer warps finished with the tile
-  unsigned int excl_ready;
-  unsigned int direct_mask;     // warps that wrote straight to global
-  unsigned int pad;
-  unsigned int wc[kMaxWarps];   // per-warp match counts, ~0u = running
+// Per ring slot: what the staged bytes are.
+struct SlotInfo {
+  unsigned long long slice;     // owning slice
+  unsigned long long t0, t1;    // samples [t0, t1) of this chunk
+  unsigned long long src;       // absolute offset of slot byte 0
+  unsigned int first, last;     // first / last chunk of its slice
+  unsigned int valid, pad;      // staged bytes
 };
 
 MAG_HD size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct SmemLayout {
-  size_t table, pf, map, stage, mbuf, queue, meta, bars, total;
-  uint32_t stage_bytes;
+  size_t table, pf, map, slots, info, queue, bars, total;
 };
 
-MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint64_t tile_bytes, uint32_t halo,
-                              uint32_t stages, uint32_t nwarps, uint32_t mbuf) {
+MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,
+                              uint32_t nwarps) {
   SmemLayout L;
   size_t o = 0;
   L.table = o;
@@ -132,17 +138,14 @@ MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint64_t tile_bytes, uint32_t h
   o += align16((size_t(1) << p.pf_bits) / 8);
   L.map = o;
   o += 256;
-  L.stage_bytes = static_cast<uint32_t>(align16(tile_bytes + halo + 32));
-  L.stage = o;
-  o += size_t(stages) * L.stage_bytes;
-  L.mbuf = o;
-  o += size_t(stages) * nwarps * mbuf * 8;
+  L.slots = o;
+  o += size_t(nwarps) * ring * slot_bytes;
+  L.info = o;
+  o += align16(size_t(nwarps) * ring * sizeof(SlotInfo));
   L.queue = o;
   o += align16(size_t(nwarps) * kQueueCap * 4);
-  L.meta = o;
-  o += align16(size_t(stages) * sizeof(StageMeta));
   L.bars = o;
-  o += size_t(stages) * 2 * 8;
+  o += size_t(nwarps) * ring * 8;
   L.total = o;
   return L;
 }

@@ -1,24 +1,26 @@
 // B200 (sm_100a) search kernels for the MAG multiple pattern matcher.
 //
-// One persistent, warp-specialised kernel fuses the reference's three search
-// stages over each text tile:
+// One persistent kernel fuses the reference's three search stages:
 //   stage 1  q-gram formation       (encode_gram_at qgram.hpp:30-36, or the
-//                                     hashed q-gram alphabet of §3.3)
+//                                     hashed q-gram alphabet of paper §3.3)
 //   stage 2  superimposed Shift-Or   (FilterMachine::scan_range
 //            over k alignments        filter.hpp:51-74, closed form)
 //   stage 3  window verification     (candidate_window / verify_window
 //            + ordered output          verify.hpp:21-31, sort_dedup :37-38)
 //
-// Data movement: a producer warp streams text tiles (+ halo) into a ring of
-// shared-memory stages with 1-D TMA bulk copies (cp.async.bulk + mbarrier
-// complete_tx); consumer warps each own a contiguous slice of a tile.  The
-// mask table, the verification prefilter and the byte map live in shared
-// memory for the whole launch.  Candidates never leave the SM: they are
-// compacted with warp ballots/scans into a per-warp queue and verified from
-// the staged bytes against a hashed pattern table.  Matches come out already
-// in (offset, pattern) order: each tile's total is published through a
-// decoupled look-back, and the tile's matches are written at their final
-// position, so no sort/merge pass is needed.
+// Every warp is an independent scanner.  It takes slices of the sample
+// stream with an atomic ticket and streams each slice through its own ring
+// of shared-memory slots with 1-D TMA bulk copies (cp.async.bulk, completion
+// on a per-slot mbarrier) — no block-level synchronisation after setup.
+// The mask table, the verification prefilter and the byte map live in
+// shared memory for the whole launch.  One sample per lane: the closed form
+// of the packed Shift-Or, D_t = OR_i mask(t-i) << i, takes the previous
+// samples' masks from neighbouring lanes (shuffles).  Hits become candidate
+// windows in a per-warp queue (warp-scan order = text order); windows are
+// verified as (window, start) pairs spread over the lanes, against a
+// shared-memory prefilter and then the hashed pattern table in global
+// memory.  Matches leave the warp already in (offset, pattern) order into
+// the slice's staging area; mag_compact_kernel concatenates the slices.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -32,9 +34,6 @@ namespace {
 std::atomic<unsigned long long> g_launches{0};
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr unsigned long long kFlagA = 1ull << 62;  // aggregate published
-constexpr unsigned long long kFlagP = 2ull << 62;  // inclusive prefix published
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -43,9 +42,6 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
                : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
@@ -69,25 +65,10 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
-__device__ __forceinline__ uint32_t warp_sum32(uint32_t v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  return v;
-}
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane) {
   uint32_t x = v;
 #pragma unroll
@@ -111,79 +92,160 @@ __device__ __forceinline__ int top_bit(E v) {
     return 31 - __clz(static_cast<int>(v));
 }
 
-// ----------------------------------------------------------- look-back
-// Exclusive prefix of `tile` over the published statuses of its
-// predecessors (decoupled look-back).  Warp-collective; all lanes return it.
-__device__ unsigned long long lookback_excl(const unsigned long long* status, long long tile,
-                                            int lane) {
-  unsigned long long excl = 0;
-  long long j = tile - 1;
-  while (j >= 0) {
-    long long idx = j - lane;
-    unsigned long long v = idx >= 0 ? ld_acquire(status + idx) : kFlagP;
-    unsigned flag = static_cast<unsigned>(v >> 62);
-    unsigned zero = __ballot_sync(kFull, flag == 0);
-    unsigned pm = __ballot_sync(kFull, flag == 2);
-    unsigned lim = kFull;
-    if (pm) {
-      int first = __ffs(pm) - 1;
-      lim = first == 31 ? kFull : ((1u << (first + 1)) - 1);
-    }
-    if (zero & lim) {
-      __nanosleep(64);
-      continue;
-    }
-    unsigned long long val = ((lim >> lane) & 1u) ? (v & kValMask) : 0ull;
-    excl += warp_sum64(val);
-    if (pm) break;
-    j -= 32;
-  }
-  return excl;
-}
-
-// ------------------------------------------------------------- kernel
-struct Smem {
-  const void* table;          // smem table (or null)
-  const uint32_t* pf;         // prefilter bitmap
-  const uint8_t* map;         // byte map
-  uint8_t* stage;             // stage buffers
-  uint64_t* mbuf;             // match buffers [stage][warp][mbuf]
-  uint32_t* queue;            // per-warp window queue
-  StageMeta* meta;
-  uint64_t* full;
-  uint64_t* empty;
-  uint32_t stage_bytes;
-};
-
-__host__ __device__ inline SmemLayout make_layout(const ScanArgs& a) {
-  return smem_layout(a.plan, a.tile_bytes, a.halo, a.stages, a.nwarps, a.mbuf);
+template <typename E>
+__device__ __forceinline__ uint32_t popc_e(E v) {
+  if constexpr (sizeof(E) == 8)
+    return __popcll(static_cast<unsigned long long>(v));
+  else
+    return __popc(static_cast<uint32_t>(v));
 }
 
 // Gram formation modes for the kernel template.
 enum KGram : int { kKExact = 0, kKHashed = 1, kKCodes = 2 };
 
+struct Smem {
+  const void* table;  // smem table (or null)
+  const uint32_t* pf;
+  const uint8_t* map;
+  uint8_t* slots;     // [warp][ring][slot_bytes]
+  SlotInfo* info;     // [warp][ring]
+  uint32_t* queue;    // [warp][kQueueCap]
+  uint64_t* bars;     // [warp][ring]
+};
+
 template <int GM, typename E, bool TSMEM, int QW>
 struct Scanner {
   const ScanArgs& A;
   const Smem& S;
-  int lane, warp;
-  // per-warp tile state
-  const uint8_t* sb;            // stage base (== text[A0])
-  const uint32_t* sw;           // stage as words
-  long long A0;                 // first byte of the tile
-  uint64_t stage_valid;         // staged bytes [A0, A0+stage_valid)
-  uint64_t* buf;                // this warp's match buffer for the stage
-  StageMeta* meta;
-  long long tile;
-  uint32_t bn;                  // matches in buf
-  bool direct;
-  unsigned long long dbase, written;
-  unsigned long long cands;     // candidate counter (this warp, whole launch)
-  long long own_lo, own_hi;     // owned start offsets, clipped to [0, n-m]
-  long long S0;                 // first super position of the tile
+  const int lane, warp;
+  uint8_t* myslots;
+  SlotInfo* myinfo;
+  uint64_t* mybars;
+  uint32_t* queue;
+  // chunk being processed
+  const uint8_t* sb;            // slot bytes (== text[src])
+  const uint32_t* sw;
+  unsigned long long src;       // absolute offset of sb[0]
+  uint32_t valid;               // staged bytes
+  // slice output
+  uint64_t* out;                // staging of the current slice
+  uint32_t fill;                // matches written for the current slice
+  unsigned long long cands;
+  // loader state (warp-uniform)
+  unsigned long long ld_slice, ld_t, ld_tend;
+  bool ld_done;
+  uint32_t loads, cons;
+  long long last_start;         // n - m: starts must be <= this
+  uint32_t cslot, lslot;        // ring slots of the next consume / load
+  // plan constants
+  uint32_t qk;                  // text bytes per sample (strided q*k, else 1)
+  uint32_t W, invW;             // starts per candidate window, 2^16/W rounded up
+  int mp, ov, lead, adv, k;
+  uint32_t inv_mp;              // bit / m' == (bit * inv_mp) >> 16
 
   __device__ Scanner(const ScanArgs& a, const Smem& s, int l, int w)
-      : A(a), S(s), lane(l), warp(w), cands(0) {}
+      : A(a), S(s), lane(l), warp(w), fill(0), cands(0) {
+    const ScanPlan& P = A.plan;
+    qk = P.overlapping || P.verify_all ? 1u : P.q * P.k;
+    W = P.overlapping ? 1u : P.q;
+    invW = (65536u + W - 1) / W;
+    mp = static_cast<int>(P.m_prime);
+    ov = mp - 1;
+    lead = mp <= 16 ? ov : 0;
+    adv = 32 - lead;
+    k = static_cast<int>(P.k);
+    inv_mp = (65536u + P.m_prime - 1) / P.m_prime;
+    cslot = lslot = 0;
+    myslots = S.slots + static_cast<size_t>(w) * A.ring * A.slot_bytes;
+    myinfo = S.info + static_cast<size_t>(w) * A.ring;
+    mybars = S.bars + static_cast<size_t>(w) * A.ring;
+    queue = S.queue + static_cast<size_t>(w) * kQueueCap;
+    ld_slice = 0;
+    ld_t = ld_tend = 0;
+    ld_done = false;
+    loads = cons = 0;
+    last_start = static_cast<long long>(A.n) - static_cast<long long>(A.plan.m);
+  }
+
+  // ------------------------------------------------------------- loader
+  // Bytes a chunk of samples [t0, t1) needs: the grams of its samples (and
+  // of the m'-1 samples before), the candidate windows they can raise (up
+  // to q*k*ov + q - 1 bytes before its first gram) and the pattern reach.
+  __device__ __forceinline__ void chunk_window(unsigned long long t0, unsigned long long t1,
+                                               unsigned long long* lo, unsigned long long* hi) const {
+    const ScanPlan& P = A.plan;
+    const long long ov = static_cast<long long>(P.m_prime) - 1;
+    long long l, h;
+    if (P.verify_all) {
+      l = static_cast<long long>(t0);
+      h = static_cast<long long>(t1) + A.back;
+    } else if (P.overlapping) {
+      l = static_cast<long long>(t0) - ov;
+      h = static_cast<long long>(t1) + P.q + A.back;
+    } else {
+      const long long qk = static_cast<long long>(P.q) * P.k;
+      l = (static_cast<long long>(t0) - ov) * qk - (static_cast<long long>(P.q) - 1);
+      h = static_cast<long long>(t1) * qk + A.back;
+    }
+    if (l < 0) l = 0;
+    l &= ~15ll;
+    if (h > static_cast<long long>(A.n)) h = static_cast<long long>(A.n);
+    if (h < l) h = l;
+    *lo = static_cast<unsigned long long>(l);
+    *hi = static_cast<unsigned long long>(h);
+  }
+
+  // Issue the next chunk of this warp's stream into slot loads % ring.
+  // Returns false when the warp has no more work.  Warp-uniform.
+  __device__ bool issue() {
+    while (!ld_done && ld_t >= ld_tend) {
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(A.ticket, 1ull);
+      x = __shfl_sync(kFull, x, 0) + A.slice_begin;
+      if (x >= A.slice_end) {
+        ld_done = true;
+        break;
+      }
+      ld_slice = x;
+      ld_t = x * A.slice_samples;
+      ld_tend = ld_t + A.slice_samples;
+      if (ld_tend > A.samples) ld_tend = A.samples;
+      if (ld_t >= ld_tend && lane == 0) A.slice_count[x] = 0;  // slice past the last sample
+    }
+    if (ld_done) return false;
+    const unsigned long long t0 = ld_t;
+    unsigned long long t1 = t0 + A.chunk_samples;
+    if (t1 > ld_tend) t1 = ld_tend;
+    unsigned long long lo, hi;
+    chunk_window(t0, t1, &lo, &hi);
+    const uint32_t slot = lslot;
+    lslot = lslot + 1 == A.ring ? 0 : lslot + 1;
+    // whole 16-byte blocks except at the very end of the text
+    const unsigned long long hi16 = (hi + 15) & ~15ull;
+    const unsigned long long bulk_end = hi16 <= A.n ? hi16 : (A.n & ~15ull);
+    const uint32_t bulk = bulk_end > lo ? static_cast<uint32_t>(bulk_end - lo) : 0u;
+    const uint32_t len = static_cast<uint32_t>(hi - lo) > bulk ? static_cast<uint32_t>(hi - lo) : bulk;
+    uint8_t* dst = myslots + static_cast<size_t>(slot) * A.slot_bytes;
+    if (static_cast<uint32_t>(lane) < len - bulk) dst[bulk + lane] = __ldg(A.text + lo + bulk + lane);
+    __syncwarp();
+    if (lane == 0) {
+      SlotInfo& in = myinfo[slot];
+      in.slice = ld_slice;
+      in.t0 = t0;
+      in.t1 = t1;
+      in.src = lo;
+      in.first = t0 == ld_slice * A.slice_samples;
+      in.last = t1 == ld_tend;
+      in.valid = len;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(mybars + slot, bulk);
+      if (bulk) tma_load_1d(dst, A.text + lo, bulk, mybars + slot);
+    }
+    __syncwarp();
+    ld_t = t1;
+    ++loads;
+    return true;
+  }
 
   // ----------------------------------------------------------- stage 1+2
   __device__ __forceinline__ E table_entry(uint32_t idx) const {
@@ -195,57 +257,54 @@ struct Scanner {
     } else {
       const uint32_t* t = TSMEM ? static_cast<const uint32_t*>(S.table)
                                 : static_cast<const uint32_t*>(A.table);
-      uint32_t word = TSMEM ? t[idx >> (5 - el)] : __ldg(t + (idx >> (5 - el)));
-      uint32_t sh = (idx & ((32u >> el) - 1u)) << el;
-      return word >> sh;
+      const uint32_t word = TSMEM ? t[idx >> (5 - el)] : __ldg(t + (idx >> (5 - el)));
+      return word >> ((idx & ((32u >> el) - 1u)) << el);
     }
   }
 
-  // Mask index of the gram read by sample t.
-  __device__ __forceinline__ uint32_t gram_index(long long t) const {
+  // Mask of the gram at slot offset rel, read by sample t (absolute; used
+  // for SMAG's code array).
+  __device__ __forceinline__ E gram_mask(uint32_t rel, unsigned long long t) const {
     const ScanPlan& P = A.plan;
-    const long long u = P.overlapping ? t : (t + 1) * (long long)P.k - 1;
     if constexpr (GM == kKCodes) {
-      return __ldg(A.codes + u);
+      const unsigned long long u = P.overlapping ? t : (t + 1) * P.k - 1;
+      return table_entry(__ldg(A.codes + u));
+    } else if constexpr (GM == kKHashed) {
+      const uint32_t wi = rel >> 2, sh = (rel & 3u) << 3;
+      uint32_t w[QW + 1];
+#pragma unroll
+      for (int i = 0; i <= QW; ++i) w[i] = sw[wi + i];
+      uint32_t x[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < QW; ++i) x[i] = __funnelshift_r(w[i], w[i + 1], sh);
+      const uint32_t rem = P.q - 4u * (QW - 1);  // 1..4 bytes in the last word
+      x[QW - 1] &= rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
+      return table_entry(hash_gram_words(x[0], x[1], x[2], x[3]) >> (32 - P.table_bits));
     } else {
-      const uint32_t rel = static_cast<uint32_t>((P.overlapping ? u : u * (long long)P.q) - A0);
-      if constexpr (GM == kKHashed) {
-        const uint32_t wi = rel >> 2, sh = (rel & 3u) << 3;
-        uint32_t w[QW + 1];
-#pragma unroll
-        for (int i = 0; i <= QW; ++i) w[i] = sw[wi + i];
-        uint32_t x[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < QW; ++i) x[i] = __funnelshift_r(w[i], w[i + 1], sh);
-        const uint32_t q = P.q;
-        // zero bytes past q in the last word
-        const uint32_t rem = q - 4u * (QW - 1);  // 1..4 bytes in the last word
-        x[QW - 1] &= rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
-        return hash_gram_words(x[0], x[1], x[2], x[3]) >> (32 - P.table_bits);
-      } else {
-        const uint32_t q = P.q, sp = P.sigma_prime;
-        uint32_t code = S.map[sb[rel + q - 1]];
-        for (int i = static_cast<int>(q) - 2; i >= 0; --i) code = code * sp + S.map[sb[rel + i]];
-        return code;
-      }
+      const uint32_t q = P.q, sp = P.sigma_prime;
+      uint32_t code = S.map[sb[rel + q - 1]];
+      for (int i = static_cast<int>(q) - 2; i >= 0; --i) code = code * sp + S.map[sb[rel + i]];
+      return table_entry(code);
     }
-  }
-
-  __device__ __forceinline__ E mask_at(long long t, long long t_last) const {
-    if (t < 0 || t > t_last) return static_cast<E>(~E(0));
-    return table_entry(gram_index(t));
   }
 
   // ----------------------------------------------------------- stage 3
-  __device__ __forceinline__ uint32_t byte_at(long long x) const {
-    return sb[static_cast<uint32_t>(x - A0)];
-  }
-
-  __device__ __forceinline__ uint32_t key_direct(long long a) const {
+  __device__ __forceinline__ uint32_t key_at(uint32_t r) const {
+    const uint32_t wi = r >> 2, sh = (r & 3u) << 3;
     const uint32_t v = A.plan.key_len;
-    uint32_t h = 0;
-    for (uint32_t i = 0; i < v; ++i) h = h * kKeyBase + byte_at(a + i);
-    return h;
+    const uint32_t w0 = sw[wi], w1 = sw[wi + 1];
+    const uint32_t x0 = __funnelshift_r(w0, w1, sh) & key_word_mask(v, 0);
+    uint32_t x1 = 0, x2 = 0, x3 = 0;
+    if (v > 4) {
+      const uint32_t w2 = sw[wi + 2];
+      x1 = __funnelshift_r(w1, w2, sh) & key_word_mask(v, 1);
+      if (v > 8) {
+        const uint32_t w3 = sw[wi + 3];
+        x2 = __funnelshift_r(w2, w3, sh) & key_word_mask(v, 2);
+        if (v > 12) x3 = __funnelshift_r(w3, sw[wi + 4], sh) & key_word_mask(v, 3);
+      }
+    }
+    return key_words(x0, x1, x2, x3);
   }
 
   __device__ __forceinline__ bool prefilter_pass(uint32_t key) const {
@@ -255,303 +314,169 @@ struct Scanner {
     return ((S.pf[i1 >> 5] >> (i1 & 31)) & (S.pf[i2 >> 5] >> (i2 & 31)) & 1u) != 0;
   }
 
-  // Exact byte comparison of pattern pid at text offset a (a+len <= n given).
-  __device__ bool equal_at(long long a, uint32_t pid, uint32_t len) const {
+  // Exact comparison of pattern pid (len bytes) with the text at slot
+  // offset r (a + len <= n is checked by the caller).
+  __device__ bool equal_at(uint32_t r, uint32_t pid, uint32_t len) const {
     const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
-    const uint64_t rel = static_cast<uint64_t>(a - A0);
-    if (rel + len <= stage_valid) {
-      const uint32_t wi = static_cast<uint32_t>(rel >> 2), sh = static_cast<uint32_t>(rel & 3) << 3;
-      const uint32_t* pw = reinterpret_cast<const uint32_t*>(p);
-      for (uint32_t i = 0; i < len; i += 4) {
-        uint32_t tw = __funnelshift_r(sw[wi + (i >> 2)], sw[wi + (i >> 2) + 1], sh);
-        uint32_t pv = __ldg(pw + (i >> 2));
-        uint32_t rem = len - i;
-        uint32_t msk = rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
-        if ((tw ^ pv) & msk) return false;
+    if (r + len <= valid) {
+      const uint32_t wi = r >> 2, sh = (r & 3u) << 3;
+      const uint4* pv4 = reinterpret_cast<const uint4*>(p);
+      for (uint32_t i = 0; i < len; i += 16) {
+        const uint4 pv = __ldg(pv4 + (i >> 4));
+        const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t o = i + 4 * j;
+          if (o >= len) break;
+          const uint32_t tw = __funnelshift_r(sw[wi + (o >> 2)], sw[wi + (o >> 2) + 1], sh);
+          const uint32_t rem = len - o;
+          const uint32_t msk = rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
+          if ((tw ^ pw[j]) & msk) return false;
+        }
       }
       return true;
     }
-    const uint8_t* t = A.text + a;
+    const uint8_t* t = A.text + src + r;
     for (uint32_t i = 0; i < len; ++i)
       if (__ldg(t + i) != __ldg(p + i)) return false;
     return true;
   }
 
-  // Number of patterns matching at a whose key hash is `key`.
-  __device__ uint32_t probe_count(long long a, uint32_t key) const {
+  // Patterns matching at slot offset r with key `key`: counted, or written
+  // (dst != nullptr) as packed keys in pattern order from dst[idx].
+  __device__ uint32_t probe(uint32_t r, uint32_t key, uint64_t* dst, uint32_t idx) const {
     const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
     const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
+    const unsigned long long a = src + r;
     uint32_t c = 0;
     for (uint32_t e = lo; e < hi; ++e) {
-      uint2 ent = __ldg(A.bucket_entries + e);
+      const uint2 ent = __ldg(A.bucket_entries + e);
       if (ent.x != key) continue;
-      uint32_t len = __ldg(A.pat_len + ent.y);
-      if (static_cast<uint64_t>(a) + len > A.n) continue;
-      if (equal_at(a, ent.y, len)) ++c;
+      const uint32_t len = __ldg(A.pat_len + ent.y);
+      if (a + len > A.n || !equal_at(r, ent.y, len)) continue;
+      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, ent.y);
+      ++c;
     }
     return c;
   }
 
-  // Ordered emission of this warp's matches for one batch.
-  __device__ void emit_matches(uint32_t cnt, long long a0, uint32_t flagged) {
-    const uint32_t excl = warp_excl_scan(cnt, lane);
-    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
-    if (total == 0) return;
-    if (!direct && bn + total > A.mbuf) enter_direct();
-    uint32_t pos = excl;
-    while (flagged) {
-      const int d = __ffs(flagged) - 1;
-      flagged &= flagged - 1;
-      const long long a = a0 + d;
-      const uint32_t key = key_mix(key_direct(a));
-      const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
-      const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
-      for (uint32_t e = lo; e < hi; ++e) {
-        uint2 ent = __ldg(A.bucket_entries + e);
-        if (ent.x != key) continue;
-        uint32_t len = __ldg(A.pat_len + ent.y);
-        if (static_cast<uint64_t>(a) + len > A.n) continue;
-        if (!equal_at(a, ent.y, len)) continue;
-        const uint64_t k = pack_match(static_cast<uint64_t>(a), ent.y);
-        if (direct) {
-          const unsigned long long idx = dbase + written + pos;
-          if (idx < A.out_cap) A.out[idx] = k;
-        } else {
-          buf[bn + pos] = k;
-        }
-        ++pos;
-      }
+  // One start per lane (lane order = text order): count, then ordered write.
+  __device__ __forceinline__ void verify_batch(bool act, long long a) {
+    uint32_t key = 0, c = 0;
+    const uint32_t r = static_cast<uint32_t>(a - static_cast<long long>(src));
+    if (act) {
+      key = key_at(r);
+      if (prefilter_pass(key)) c = probe(r, key, nullptr, 0);
     }
-    if (direct)
-      written += total;
-    else
-      bn += total;
-    __syncwarp();
+    if (!__any_sync(kFull, c != 0)) return;
+    const uint32_t excl = warp_excl_scan(c, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + c, 31);
+    if (c) probe(r, key, out, fill + excl);
+    fill += total;
   }
 
-  // Verifies windows [a0, a0+W) (one per lane), clipped to the owned starts.
-  __device__ void verify_windows(bool active, long long a0, uint32_t W) {
-    uint32_t cnt = 0, flagged = 0;
-    if (active) {
-      long long lo = a0 < own_lo ? own_lo : a0;
-      long long hi = a0 + W - 1 > own_hi - 1 ? own_hi - 1 : a0 + W - 1;
-      if (lo <= hi) {
-        const uint32_t v = A.plan.key_len;
-        uint32_t h = key_direct(lo);
-        const uint32_t pw = A.plan.key_pow;
-        for (long long a = lo;; ++a) {
-          const uint32_t key = key_mix(h);
-          if (prefilter_pass(key)) {
-            uint32_t c = probe_count(a, key);
-            if (c) {
-              cnt += c;
-              flagged |= 1u << static_cast<uint32_t>(a - a0);
-            }
-          }
-          if (a == hi) break;
-          h = (h - byte_at(a) * pw) * kKeyBase + byte_at(a + v);
-        }
-      }
-    }
-    if (__any_sync(kFull, cnt != 0)) emit_matches(cnt, a0, flagged);
-  }
-
-  // ------------------------------------------------------ output protocol
-  __device__ void enter_direct() {
-    // Exclusive prefix of the tile, then of this warp inside the tile.
-    unsigned long long excl;
-    if (*(volatile unsigned int*)&meta->excl_ready) {
-      excl = *(volatile unsigned long long*)&meta->excl;
-    } else {
-      excl = lookback_excl(A.status, tile, lane);
-      if (lane == 0) {
-        *(volatile unsigned long long*)&meta->excl = excl;
-        __threadfence_block();
-        *(volatile unsigned int*)&meta->excl_ready = 1;
-      }
-    }
-    uint32_t mine = 0;
-    if (lane < warp) {
-      volatile unsigned int* wc = &meta->wc[lane];
-      unsigned int v;
-      while ((v = *wc) == 0xffffffffu) __nanosleep(32);
-      mine = v;
-    }
+  // Verify the queued windows: (window, start) pairs spread over the lanes
+  // in order, so each lane checks one start.  Entries are super positions
+  // relative to ss_ref.
+  __device__ void drain(uint32_t qlen, long long ss_ref) {
     __syncwarp();
-    __threadfence_block();
-    dbase = excl + warp_sum32(mine);
-    if (lane == 0) atomicOr(&meta->direct_mask, 1u << warp);
-    for (uint32_t i = lane; i < bn; i += 32) {
-      const unsigned long long idx = dbase + i;
-      if (idx < A.out_cap) A.out[idx] = buf[i];
-    }
-    written = bn;
-    bn = 0;
-    direct = true;
-    __syncwarp();
-  }
-
-  __device__ void finish_tile(int s) {
-    const uint32_t count = direct ? static_cast<uint32_t>(written) : bn;
-    unsigned int old = 0;
-    if (lane == 0) {
-      *(volatile unsigned int*)&meta->wc[warp] = count;
-      __threadfence_block();
-      old = atomicAdd(&meta->done, 1u);
-      __threadfence_block();
-    }
-    old = __shfl_sync(kFull, old, 0);
-    if (old != A.nwarps - 1) return;
-    // Last warp of the tile: publish, look back, flush the buffered warps.
-    uint32_t wv = lane < static_cast<int>(A.nwarps) ? *(volatile unsigned int*)&meta->wc[lane] : 0;
-    const unsigned long long agg = warp_sum32(wv);
-    unsigned long long excl;
-    if (tile == 0) {
-      excl = 0;
-    } else if (*(volatile unsigned int*)&meta->excl_ready) {
-      excl = *(volatile unsigned long long*)&meta->excl;
-    } else {
-      if (lane == 0) st_release(A.status + tile, kFlagA | agg);
-      excl = lookback_excl(A.status, tile, lane);
-    }
-    if (lane == 0) {
-      st_release(A.status + tile, kFlagP | (excl + agg));
-      if (static_cast<unsigned long long>(tile) == A.num_tiles - 1) A.counters[2] = excl + agg;
-    }
-    const unsigned int dmask = *(volatile unsigned int*)&meta->direct_mask;
-    unsigned long long run = excl;
-    const uint64_t* sbuf = S.mbuf + static_cast<size_t>(s) * A.nwarps * A.mbuf;
-    for (uint32_t v = 0; v < A.nwarps; ++v) {
-      const uint32_t c = *(volatile unsigned int*)&meta->wc[v];
-      if (!((dmask >> v) & 1u)) {
-        const uint64_t* src = sbuf + static_cast<size_t>(v) * A.mbuf;
-        for (uint32_t i = lane; i < c; i += 32) {
-          const unsigned long long idx = run + i;
-          if (idx < A.out_cap) A.out[idx] = src[i];
-        }
+    const uint32_t pairs = qlen * W;
+    for (uint32_t p0 = 0; p0 < pairs; p0 += 32) {
+      const uint32_t p = p0 + lane;
+      bool act = p < pairs;
+      long long a = 0;
+      if (act) {
+        const uint32_t ci = (p * invW) >> 16;
+        const uint32_t d = p - ci * W;
+        const long long ss = static_cast<long long>(queue[ci]) + ss_ref;
+        a = ss * static_cast<long long>(W) - static_cast<long long>(W - 1) + d;
+        act = a >= 0 && a <= last_start;
       }
-      run += c;
+      verify_batch(act, a);
     }
     __syncwarp();
   }
 
-  // ------------------------------------------------------ one tile slice
-  __device__ void process(int s, long long tile_id) {
+  // ------------------------------------------------------------ a chunk
+  __device__ void process_chunk(const SlotInfo& in) {
     const ScanPlan& P = A.plan;
-    tile = tile_id;
-    meta = S.meta + s;
-    sb = S.stage + static_cast<size_t>(s) * S.stage_bytes;
-    sw = reinterpret_cast<const uint32_t*>(sb);
-    A0 = tile * static_cast<long long>(A.tile_bytes);
-    const long long n = static_cast<long long>(A.n);
-    long long A1 = A0 + static_cast<long long>(A.tile_bytes);
-    if (A1 > n) A1 = n;
-    stage_valid = static_cast<uint64_t>(
-        (A0 + A.tile_bytes + A.halo > A.n ? A.n : A0 + A.tile_bytes + A.halo) - A0);
-    buf = S.mbuf + (static_cast<size_t>(s) * A.nwarps + warp) * A.mbuf;
-    bn = 0;
-    direct = false;
-    written = 0;
-
-    const long long gs = P.overlapping ? 1 : P.q;
-    const long long Wn = P.overlapping ? 1 : P.q;  // starts per window
-    S0 = A0 / gs;
-    const long long S1 = (A1 == n) ? (n + gs - 1) / gs : A1 / gs;
-    const long long span = S1 - S0;
-    const long long s_lo = S0 + span * warp / A.nwarps;
-    const long long s_hi = S0 + span * (warp + 1) / A.nwarps;
-    own_lo = s_lo * gs;
-    own_hi = (warp == static_cast<int>(A.nwarps) - 1) ? A1 : s_hi * gs;
-    const long long last_start = n - static_cast<long long>(P.m);  // inclusive
-    if (own_hi > last_start + 1) own_hi = last_start + 1;
-
+    const int nsamp = static_cast<int>(in.t1 - in.t0);
     if (P.verify_all) {
-      // Every start is a candidate (q = k = m' = 1 with an all-admitting
-      // table): windows of 16 consecutive starts, one per lane.
-      for (long long base = own_lo; base < own_hi; base += 32 * 16) {
-        const long long a0 = base + 16LL * lane;
-        verify_windows(a0 < own_hi, a0, 16);
+      // every start is a candidate: one start per lane, in order
+      const long long t0 = static_cast<long long>(in.t0);
+      for (int b = 0; b < nsamp; b += 32) {
+        const long long a = t0 + b + lane;
+        verify_batch(b + lane < nsamp && a <= last_start, a);
       }
-    } else if (s_lo < s_hi) {
-      scan_slice(s_lo, s_hi, gs, Wn);
+      return;
     }
-    finish_tile(s);
-  }
-
-  // Filter the slice's samples, queue candidate windows in order, verify.
-  __device__ void scan_slice(long long s_lo, long long s_hi, long long gs, long long Wn) {
-    const ScanPlan& P = A.plan;
-    const int mp = static_cast<int>(P.m_prime);
-    const int ov = mp - 1;
-    const long long k = P.k;
-    const long long T = static_cast<long long>(A.samples);
-    // verified super positions: [s_lo, s_ver]; counted: [s_lo, s_hi)
-    const long long s_ver = P.overlapping ? s_hi - 1 : s_hi;
-    long long t_first, t_last;
-    if (P.overlapping) {
-      t_first = s_lo + ov;
-      t_last = s_ver + ov;
-    } else {
-      t_first = s_lo / k + ov;
-      t_last = s_ver / k + ov;
-    }
-    if (t_last > T - 1) t_last = T - 1;
-    if (t_first > t_last) return;
-    uint32_t* queue = S.queue + warp * kQueueCap;
-    uint32_t qlen = 0;
+    // slot offset of the gram of relative sample 0, and per-sample stride
+    const int g0 = static_cast<int>(
+        (P.overlapping ? in.t0 : ((in.t0 + 1) * P.k - 1) * P.q) - src);
+    const int gstep = static_cast<int>(qk);
+    // super positions: ss = ss_ref + rel, rel = tr * k + (k - 1 - j) >= 0
+    const long long ss_ref = (static_cast<long long>(in.t0) - ov) * k;
+    // samples before the text start have no gram; samples < m'-1 never hit
+    const int tmin = in.t0 < static_cast<unsigned long long>(ov) ? -static_cast<int>(in.t0) : -ov;
+    const int thit = in.t0 < static_cast<unsigned long long>(ov) ? ov - static_cast<int>(in.t0) : 0;
     const E mm = static_cast<E>(P.match_mask);
-    const bool shuffle_path = mp <= 16;
-    const long long adv = shuffle_path ? 32 - ov : 32;
-    const long long start = shuffle_path ? t_first - ov : t_first;
-    for (long long base = start; base + (shuffle_path ? ov : 0) <= t_last; base += adv) {
-      const long long t = base + lane;
+    const E ones = static_cast<E>(~E(0));
+    uint32_t qlen = 0;
+    for (int base = -lead; base + lead < nsamp; base += adv) {
+      const int tr = base + lane;
       E D;
-      if (shuffle_path) {
-        const E M = mask_at(t, t_last);
+      if (mp <= 16) {
+        const E M = (tr >= tmin && tr < nsamp) ? gram_mask(static_cast<uint32_t>(g0 + tr * gstep), in.t0 + tr) : ones;
         D = M;
         for (int i = 1; i <= ov; ++i) D |= static_cast<E>(shfl_up_e(M, i) << i);
       } else {
         D = static_cast<E>(0);
-        for (int i = 0; i < mp; ++i) D |= static_cast<E>(mask_at(t - i, t_last) << i);
-      }
-      E hits = static_cast<E>(0);
-      const bool out_lane = (shuffle_path ? lane >= ov : true) && t >= t_first && t <= t_last;
-      if (out_lane) hits = static_cast<E>(~D) & mm;
-      // candidates of this lane, ascending super position (alignment j descending)
-      uint32_t cnt = 0;
-      long long ss_base = P.overlapping ? t - ov : (t - ov) * k;
-      {
-        E h = hits;
-        while (h) {
-          const int bit = top_bit(h);
-          h &= static_cast<E>(~(E(1) << bit));
-          const long long j = bit / mp;
-          const long long ss = P.overlapping ? ss_base : ss_base + (k - 1 - j);
-          if (ss < s_lo || ss > s_ver) continue;
-          if (ss < s_hi) ++cands;
-          ++cnt;
+        for (int i = 0; i < mp; ++i) {
+          const int ti = tr - i;
+          const E M = (ti >= tmin && ti < nsamp) ? gram_mask(static_cast<uint32_t>(g0 + ti * gstep), in.t0 + ti) : ones;
+          D |= static_cast<E>(M << i);
         }
       }
+      const E hits = (lane >= lead && tr >= thit && tr < nsamp) ? static_cast<E>(~D & mm) : static_cast<E>(0);
+      const unsigned hb = __ballot_sync(kFull, hits != 0);
+      if (!hb) continue;
+      if (k == 1) {
+        // one alignment: at most one candidate per lane, ballot order
+        const uint32_t total = __popc(hb);
+        cands += hits ? 1u : 0u;
+        if (qlen + total > kQueueCap) {
+          drain(qlen, ss_ref);
+          qlen = 0;
+        }
+        if (hits) queue[qlen + __popc(hb & ((1u << lane) - 1u))] = static_cast<uint32_t>(tr);
+        __syncwarp();
+        qlen += total;
+        continue;
+      }
+      // k alignments: candidates of a lane in ascending super position
+      // (alignment j descending)
+      const uint32_t cnt = popc_e(hits);
+      cands += cnt;
       const uint32_t excl = warp_excl_scan(cnt, lane);
       const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
+      const int rel_base = tr * k + (k - 1);
       uint32_t done = 0;
       while (done < total) {
         if (qlen == kQueueCap) {
-          drain(queue, qlen, gs, Wn);
+          drain(qlen, ss_ref);
           qlen = 0;
         }
-        const uint32_t take = min(kQueueCap - qlen, total - done);
+        const uint32_t take = min(static_cast<uint32_t>(kQueueCap) - qlen, total - done);
         if (cnt) {
           uint32_t rank = excl;
           E h = hits;
           while (h) {
             const int bit = top_bit(h);
             h &= static_cast<E>(~(E(1) << bit));
-            const long long j = bit / mp;
-            const long long ss = P.overlapping ? ss_base : ss_base + (k - 1 - j);
-            if (ss < s_lo || ss > s_ver) continue;
-            if (rank >= done && rank < done + take)
-              queue[qlen + rank - done] = static_cast<uint32_t>(ss - S0);
+            if (rank >= done && rank < done + take) {
+              const int j = static_cast<int>((static_cast<uint32_t>(bit) * inv_mp) >> 16);
+              queue[qlen + rank - done] = static_cast<uint32_t>(rel_base - j);
+            }
             ++rank;
           }
         }
@@ -560,43 +485,51 @@ struct Scanner {
         done += take;
       }
     }
-    if (qlen) drain(queue, qlen, gs, Wn);
+    if (qlen) drain(qlen, ss_ref);
   }
 
-  __device__ void drain(const uint32_t* queue, uint32_t qlen, long long gs, long long Wn) {
-    __syncwarp();
-    for (uint32_t i0 = 0; i0 < qlen; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      const bool act = i < qlen;
-      long long a0 = 0;
-      if (act) {
-        const long long ss = S0 + queue[i];
-        a0 = A.plan.overlapping ? ss : gs * ss - (Wn - 1);
-      }
-      verify_windows(act, a0, static_cast<uint32_t>(Wn));
+  // ------------------------------------------------------------- driver
+  __device__ void run() {
+    for (uint32_t r = 0; r < A.ring; ++r)
+      if (!issue()) break;
+    uint32_t phase = 0;
+    while (cons < loads) {
+      const uint32_t slot = cslot;
+      mbar_wait(mybars + slot, phase);
+      cslot = cslot + 1 == A.ring ? 0 : cslot + 1;
+      phase ^= cslot == 0;
+      const SlotInfo in = myinfo[slot];
+      sb = myslots + static_cast<size_t>(slot) * A.slot_bytes;
+      sw = reinterpret_cast<const uint32_t*>(sb);
+      src = in.src;
+      valid = in.valid;
+      if (in.first) fill = 0;
+      out = A.staging + static_cast<size_t>(in.slice) * A.slice_cap;
+      process_chunk(in);
+      if (in.last && lane == 0) A.slice_count[in.slice] = fill;
+      __syncwarp();
+      ++cons;
+      issue();
     }
-    __syncwarp();
+    unsigned long long c = cands;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0 && c) atomicAdd(A.counters + 1, c);
   }
 };
 
 template <int GM, typename E, bool TSMEM, int QW>
-__global__ void __launch_bounds__((kMaxWarps + 1) * 32, 1)
-    mag_scan_kernel(const __grid_constant__ ScanArgs A) {
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const SmemLayout L = make_layout(A);
+  const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
   Smem S;
   S.table = smem + L.table;
   S.pf = reinterpret_cast<const uint32_t*>(smem + L.pf);
   S.map = smem + L.map;
-  S.stage = smem + L.stage;
-  S.mbuf = reinterpret_cast<uint64_t*>(smem + L.mbuf);
+  S.slots = smem + L.slots;
+  S.info = reinterpret_cast<SlotInfo*>(smem + L.info);
   S.queue = reinterpret_cast<uint32_t*>(smem + L.queue);
-  S.meta = reinterpret_cast<StageMeta*>(smem + L.meta);
-  S.full = reinterpret_cast<uint64_t*>(smem + L.bars);
-  S.empty = S.full + A.stages;
-  S.stage_bytes = L.stage_bytes;
-
-  // Resident tables: mask table, prefilter, byte map.
+  S.bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   {
     const int tid = threadIdx.x, nt = blockDim.x;
     if (TSMEM && A.plan.table_in_smem) {
@@ -612,65 +545,63 @@ __global__ void __launch_bounds__((kMaxWarps + 1) * 32, 1)
       for (size_t i = tid; i < nv; i += nt) dst[i] = __ldg(src + i);
     }
     for (int i = tid; i < 256; i += nt) smem[L.map + i] = A.map ? __ldg(A.map + i) : 0;
-    if (tid == 0) {
-      for (uint32_t s = 0; s < A.stages; ++s) {
-        mbar_init(S.full + s, 1);
-        mbar_init(S.empty + s, A.nwarps);
-      }
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    for (uint32_t b = tid; b < A.nwarps * A.ring; b += nt) mbar_init(S.bars + b, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
   }
+  Scanner<GM, E, TSMEM, QW> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
+  sc.run();
+}
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t NS = A.stages;
-  unsigned long long* ticket = A.ticket;
-
-  if (warp == static_cast<int>(A.nwarps)) {
-    // ---------------- producer warp: tile tickets + TMA bulk loads
-    if (lane == 0) {
-      for (uint32_t it = 0;; ++it) {
-        const uint32_t s = it % NS, ph = (it / NS) & 1u;
-        mbar_wait(S.empty + s, ph ^ 1u);
-        long long tile = static_cast<long long>(A.tile_begin + atomicAdd(ticket, 1ull));
-        if (tile >= static_cast<long long>(A.tile_end)) tile = -1;
-        StageMeta* m = S.meta + s;
-        m->tile = tile;
-        m->done = 0;
-        m->excl_ready = 0;
-        m->direct_mask = 0;
-        for (int w = 0; w < kMaxWarps; ++w) m->wc[w] = 0xffffffffu;
-        if (tile < 0) {
-          mbar_arrive(S.full + s);
-          break;
-        }
-        const uint64_t a0 = static_cast<uint64_t>(tile) * A.tile_bytes;
-        uint64_t end = a0 + A.tile_bytes + A.halo;
-        if (end > A.n) end = A.n;
-        const uint32_t len = static_cast<uint32_t>(end - a0);
-        const uint32_t bulk = len & ~15u;
-        uint8_t* dst = S.stage + static_cast<size_t>(s) * S.stage_bytes;
-        for (uint32_t i = bulk; i < len; ++i) dst[i] = __ldg(A.text + a0 + i);
-        mbar_arrive_expect_tx(S.full + s, bulk);
-        if (bulk) tma_load_1d(dst, A.text + a0, bulk, S.full + s);
-      }
+// Gather: block b owns slices [b*per, (b+1)*per); its output offset is the
+// sum of all earlier slice counts (each block reduces that prefix itself —
+// at most a few tens of thousands of words from L2), then it copies its
+// slices in order.  The last block publishes the total.
+__global__ void __launch_bounds__(1024) mag_compact_kernel(const __grid_constant__ ScanArgs A,
+                                                            uint64_t* __restrict__ out,
+                                                            uint64_t out_cap) {
+  __shared__ unsigned long long red[32];
+  __shared__ unsigned long long s_base;
+  const uint64_t ns = A.num_slices;
+  const uint64_t per = (ns + gridDim.x - 1) / gridDim.x;
+  uint64_t s0 = blockIdx.x * per;
+  if (s0 > ns) s0 = ns;
+  uint64_t s1 = s0 + per;
+  if (s1 > ns) s1 = ns;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  unsigned long long acc = 0, mx = 0;
+  for (uint64_t i = tid; i < s0; i += blockDim.x) acc += A.slice_count[i];
+  for (uint64_t i = s0 + tid; i < s1; i += blockDim.x) {
+    const unsigned long long c = A.slice_count[i];
+    mx = c > mx ? c : mx;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    acc += __shfl_xor_sync(kFull, acc, o);
+    const unsigned long long y = __shfl_xor_sync(kFull, mx, o);
+    mx = y > mx ? y : mx;
+  }
+  if (lane == 0) red[wid] = acc;
+  if (lane == 0 && mx) atomicMax(A.counters + 3, mx);
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long b = 0;
+    for (int w = 0; w < nw; ++w) b += red[w];
+    s_base = b;
+  }
+  __syncthreads();
+  unsigned long long base = s_base;
+  for (uint64_t s = s0; s < s1; ++s) {
+    const unsigned long long c = A.slice_count[s];
+    if (c) {
+      const unsigned long long cc = c < A.slice_cap ? c : A.slice_cap;
+      const uint64_t* srcp = A.staging + s * A.slice_cap;
+      for (unsigned long long i = tid; i < cc; i += blockDim.x)
+        if (base + i < out_cap) out[base + i] = srcp[i];
     }
-    return;
+    base += c;
   }
-
-  // ---------------- consumer warps
-  Scanner<GM, E, TSMEM, QW> sc(A, S, lane, warp);
-  for (uint32_t it = 0;; ++it) {
-    const uint32_t s = it % NS, ph = (it / NS) & 1u;
-    mbar_wait(S.full + s, ph);
-    const long long tile = *(volatile long long*)&S.meta[s].tile;
-    if (tile < 0) break;
-    sc.process(static_cast<int>(s), tile);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(S.empty + s);
-  }
-  const unsigned long long c = warp_sum64(sc.cands);
-  if (lane == 0 && c) atomicAdd(A.counters + 1, c);
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) A.counters[2] = base;
 }
 
 // SMAG prepare (encode_text qgram.cpp:29-37) on the device.
@@ -699,10 +630,14 @@ __global__ void mag_encode_kernel(const ScanPlan P, const uint8_t* __restrict__ 
 template <int GM, typename E, bool TSMEM, int QW>
 cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
   auto k = mag_scan_kernel<GM, E, TSMEM, QW>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  k<<<grid, (a.nwarps + 1) * 32, smem, st>>>(a);
+  static int configured_smem = -1;  // per instantiation
+  if (configured_smem != static_cast<int>(smem)) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured_smem = static_cast<int>(smem);
+  }
+  k<<<grid, a.nwarps * 32, smem, st>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -725,7 +660,7 @@ template <int GM>
 cudaError_t launch_e(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
   const bool wide = a.plan.entry_log2 == 6;
   if constexpr (GM == kKHashed) {
-    // hashed tables are always sized to shared memory
+    // hashed tables are sized to shared memory
     return wide ? launch_qw<GM, uint64_t, true>(a, st, grid, smem)
                 : launch_qw<GM, uint32_t, true>(a, st, grid, smem);
   } else {
@@ -741,16 +676,23 @@ cudaError_t launch_e(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) 
 
 LaunchShape scan_shape(const ScanArgs& a) {
   LaunchShape s;
-  s.smem_bytes = make_layout(a).total;
-  s.threads = (a.nwarps + 1) * 32;
+  s.smem_bytes = smem_layout(a.plan, a.slot_bytes, a.ring, a.nwarps).total;
+  s.threads = a.nwarps * 32;
   return s;
 }
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
-  const size_t smem = make_layout(a).total;
+  const size_t smem = smem_layout(a.plan, a.slot_bytes, a.ring, a.nwarps).total;
   if (a.plan.smag) return launch_e<kKCodes>(a, stream, grid, smem);
   if (a.plan.gram_mode == kGramHashed) return launch_e<kKHashed>(a, stream, grid, smem);
   return launch_e<kKExact>(a, stream, grid, smem);
+}
+
+cudaError_t launch_compact(const ScanArgs& a, uint64_t* out, uint64_t out_cap, cudaStream_t stream,
+                           int grid) {
+  mag_compact_kernel<<<grid, 1024, 0, stream>>>(a, out, out_cap);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,

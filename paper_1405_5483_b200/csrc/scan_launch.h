@@ -8,6 +8,13 @@
 namespace magb {
 
 // Everything one scan launch needs.  Device pointers only.
+//
+// Work decomposition: the filter's samples t in [0, samples) are cut into
+// slices of slice_samples; a slice is owned by one warp (dynamic ticket) and
+// produces the matches of exactly the candidate windows its samples raise,
+// in (offset, pattern) order, into staging + slice * slice_cap.  A slice is
+// streamed through the warp's ring of shared-memory slots in chunks of
+// chunk_samples samples (TMA bulk copies, one mbarrier per slot).
 struct ScanArgs {
   ScanPlan plan;
   const uint8_t* text;          // 16-byte aligned
@@ -21,17 +28,20 @@ struct ScanArgs {
   const uint64_t* pat_off;
   const uint32_t* pat_len;
   const uint8_t* map;           // 256-byte alphabet map (exact grams)
-  uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping
-  uint64_t tile_bytes;          // multiple of 16 and of the gram step
-  uint64_t tile_begin, tile_end;  // tiles this launch owns
-  uint64_t num_tiles;           // tiles of the whole search (status array)
-  uint32_t halo;                // extra staged bytes after a tile
-  uint32_t nwarps, stages, mbuf;
-  uint64_t* out;                // packed (offset, pid) keys
-  uint64_t out_cap;
-  unsigned long long* status;   // num_tiles look-back words (zeroed per search)
-  unsigned long long* counters; // [1] candidates, [2] matches
-  unsigned long long* ticket;   // tile ticket of this launch (zeroed)
+  uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping, n verify-all
+  uint64_t slice_samples;       // multiple of chunk_samples
+  uint32_t chunk_samples;       // samples per chunk (iterations * advance)
+  uint32_t back;                // staged bytes after the last gram (pattern reach)
+  uint32_t slot_bytes;          // one ring slot (multiple of 16)
+  uint32_t ring;                // slots per warp
+  uint32_t nwarps;              // warps per CTA
+  uint64_t slice_begin, slice_end;  // slices of this launch
+  uint64_t num_slices;
+  uint64_t* staging;            // num_slices * slice_cap packed matches
+  uint32_t slice_cap;
+  uint32_t* slice_count;        // exact per-slice counts (even past slice_cap)
+  unsigned long long* counters; // [1] candidates [2] matches [3] max slice count
+  unsigned long long* ticket;   // slice ticket of this launch (zeroed)
 };
 
 struct LaunchShape {
@@ -39,11 +49,15 @@ struct LaunchShape {
   unsigned threads;
 };
 
-// Computes the dynamic shared memory and block size of launch_scan().
 LaunchShape scan_shape(const ScanArgs& a);
 
-// Enqueues the fused filter+verify+ordered-output kernel.
+// Enqueues the fused filter + verify kernel (persistent, `grid` CTAs).
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid);
+
+// Gathers the staged slices into the sorted output (out[0..total)) and
+// writes counters[2] (total) and counters[3] (largest slice count).
+cudaError_t launch_compact(const ScanArgs& a, uint64_t* out, uint64_t out_cap, cudaStream_t stream,
+                           int grid);
 
 // SMAG prepare: codes[u] = mask index of gram u, for u < n/q.
 cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,

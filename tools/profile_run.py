@@ -1,0 +1,36 @@
+"""Minimal driver for ncu: a few device-resident searches of one config."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_1405_5483_b200 as mag  # noqa: E402
+from paper_1405_5483_b200 import workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--scale", type=float, default=1.0)
+ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--opts", default="", help="engine kwargs, e.g. tile_bytes=16384,warps=8")
+a = ap.parse_args()
+kw = {}
+for kv in filter(None, a.opts.split(",")):
+    k, v = kv.split("=")
+    kw[k] = int(v) if v.lstrip("-").isdigit() else v
+w = workloads.generate(a.config, a.scale)
+e = mag.Engine(w.patterns, **kw)
+d = torch.from_numpy(w.text).cuda()
+p = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
+s = torch.cuda.Stream()
+mag.scan_timer(True)
+for _ in range(a.iters):
+    e.search_prepared_async(p, s.cuda_stream).close()
+torch.cuda.synchronize()
+ms, n = mag.scan_timer_read()
+m = e.search_prepared(p)
+print(f"{w.name} plan={e.plan()} matches={len(m)} metrics={m.metrics()} kernel_ms={ms / max(n, 1):.3f} "
+      f"GB/s={w.text.size / (ms / max(n, 1)) / 1e6:.1f}")
