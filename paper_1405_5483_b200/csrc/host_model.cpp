@@ -203,9 +203,9 @@ bool tune(const TuningInput& in, int fixed_q, int fixed_k, TuningResult* out, st
 // ------------------------------------------------------------------ plan
 namespace {
 
-constexpr uint32_t kChunkTarget = 1024;   // gram bytes per ring slot
+constexpr uint32_t kChunkTarget = 1536;   // gram bytes per ring slot
 constexpr uint32_t kSliceTarget = 32768;  // text bytes per warp work item
-constexpr uint32_t kDefaultRing = 3;
+constexpr uint32_t kDefaultRing = 2;
 constexpr uint32_t kDefaultWarps = 16;
 
 unsigned pow2ceil_log2(unsigned x) {
@@ -240,8 +240,15 @@ double prefilter_fp(double keys, unsigned pf_bits) {
 // DESIGN.md): per sample gram+lookup, per extra m' a shuffle, per candidate
 // a queue slot, per verified start a rolled key + prefilter, per prefilter
 // pass an L2 bucket probe.
-constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 12,
-                 kCostProbe = 150, kCostVerifyAll = 16;
+constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 10, kCostStart = 45,
+                 kCostWindow = 45, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40;
+
+// Expected pattern-table entries sharing a probed key (exact byte compares)
+// when `keys` keys of v bytes are drawn over the pattern alphabet.
+double key_hits(double keys, double sigma, unsigned v) {
+  const double universe = std::pow(sigma, static_cast<double>(v));
+  return universe > 1e15 ? 0.0 : keys / universe;
+}
 
 // Chunk / slice / slot sizes of the warp-streaming kernel.
 void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
@@ -399,7 +406,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       const size_t room = room_for(1, 1, 1, 1);
       unsigned pf = 7;
       while (pf < 24 && (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
-      best.cost = kCostVerifyAll + prefilter_fp(keys, pf) * kCostProbe;
+      best.cost = kCostVerifyAll + prefilter_fp(keys, pf) * kCostProbe +
+                  key_hits(keys, sigma_obs, static_cast<unsigned>(std::min<size_t>(m, 16))) * kCostCompare;
       best.pf = pf;
       best.cpb = 1;
     }
@@ -434,8 +442,15 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                        pm * (kCostCand + kCostStart + prefilter_fp(keys, pf) * kCostProbe);
               } else {
                 cpb = pm / q;  // k alignments per sample, one sample per k*q bytes
-                cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) + cpb * kCostCand +
-                       pm * (kCostStart + prefilter_fp(keys, pf) * kCostProbe);
+                if (q > 1)     // window keys: one probe per candidate, r*q keys indexed
+                  cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) +
+                         cpb * (kCostCand + kCostWindow + prefilter_fp(keys * q, pf) * kCostProbe +
+                                key_hits(keys * q, sigma_obs,
+                                         static_cast<unsigned>(std::min<size_t>(16, m - q + 1))) *
+                                    kCostCompare);
+                else
+                  cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) + cpb * kCostCand +
+                         pm * (kCostStart + prefilter_fp(keys, pf) * kCostProbe);
               }
               if (cost < best.cost * 0.999) {
                 best.cost = cost;
@@ -506,16 +521,18 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     const size_t room = rq.smem_limit > fixed + 4096 ? rq.smem_limit - fixed - 4096 : 0;
     sp.table_in_smem = sp.table_bytes + (size_t(1) << pf) / 8 <= room;
     const size_t left = room - (sp.table_in_smem ? sp.table_bytes : 0);
-    while (pf < 22 && (size_t(1) << (pf + 1)) / 8 <= left &&
-           (size_t(1) << pf) < 16 * std::max<size_t>(pd.r, 1))
-      ++pf;
+    const size_t nkeys = std::max<size_t>(pd.r, 1) * (!sp.overlapping && sp.q > 1 ? sp.q : 1);
+    while (pf < 22 && (size_t(1) << (pf + 1)) / 8 <= left && (size_t(1) << pf) < 16 * nkeys) ++pf;
     sp.pf_bits = pf;
   } else {
     sp.table_in_smem = sp.verify_all ? 0 : 1;
   }
+  sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
+  sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
   {
+    const size_t keys = sp.window_key ? pd.r * sp.q : pd.r;
     unsigned bb = 4;
-    while ((size_t(1) << bb) < 2 * pd.r && bb < 26) ++bb;
+    while ((size_t(1) << bb) < 2 * keys && bb < 27) ++bb;
     sp.bucket_bits = bb;
   }
   // oversized rings (long patterns, wide windows): fewer warps per CTA
@@ -599,29 +616,46 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
 void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt) {
   const ScanPlan& sp = P.sp;
   const size_t r = pd.r;
-  std::vector<uint32_t> keys(r);
-  for (size_t i = 0; i < r; ++i) keys[i] = key_bytes(pd.pattern(i), sp.key_len);
+  // (key, pattern | shift << 24): one per pattern, or one per (pattern,
+  // shift) with window keys; bucket order = (shift descending, pattern
+  // ascending) so hits come out in (start, pattern) order.
+  struct Ent {
+    uint32_t key, tag;
+  };
+  std::vector<Ent> ents;
+  if (sp.window_key) {
+    ents.reserve(r * sp.q);
+    for (int s = static_cast<int>(sp.q) - 1; s >= 0; --s)
+      for (size_t i = 0; i < r; ++i)
+        ents.push_back({key_bytes(pd.pattern(i) + s, sp.wkey_len),
+                        static_cast<uint32_t>(i) | (static_cast<uint32_t>(s) << kPidBits)});
+  } else {
+    ents.reserve(r);
+    for (size_t i = 0; i < r; ++i)
+      ents.push_back({key_bytes(pd.pattern(i), sp.key_len), static_cast<uint32_t>(i)});
+  }
   // prefilter: two probes per key (scan_kernels.cu prefilter_pass)
   const size_t pf_words = std::max<size_t>(4, (size_t(1) << sp.pf_bits) / 32);
   pt->prefilter.assign(align16(pf_words * 4) / 4, 0);
-  for (size_t i = 0; i < r; ++i) {
-    const uint32_t key = keys[i];
-    const uint32_t i1 = key >> (32 - sp.pf_bits);
-    const uint32_t i2 = ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - sp.pf_bits);
-    pt->prefilter[i1 >> 5] |= 1u << (i1 & 31);
-    pt->prefilter[i2 >> 5] |= 1u << (i2 & 31);
+  if (sp.pf_bits) {
+    for (const Ent& e : ents) {
+      const uint32_t i1 = e.key >> (32 - sp.pf_bits);
+      const uint32_t i2 = ((e.key ^ (e.key >> 15)) * 0x2C1B3C6Du) >> (32 - sp.pf_bits);
+      pt->prefilter[i1 >> 5] |= 1u << (i1 & 31);
+      pt->prefilter[i2 >> 5] |= 1u << (i2 & 31);
+    }
   }
-  // buckets by low key bits; entries ordered by (bucket, pattern index)
+  // buckets by low key bits, stable within a bucket
   const size_t nb = size_t(1) << sp.bucket_bits;
   pt->bucket_start.assign(nb + 1, 0);
-  for (size_t i = 0; i < r; ++i) pt->bucket_start[(keys[i] & (nb - 1)) + 1]++;
+  for (const Ent& e : ents) pt->bucket_start[(e.key & (nb - 1)) + 1]++;
   for (size_t b = 0; b < nb; ++b) pt->bucket_start[b + 1] += pt->bucket_start[b];
   std::vector<uint32_t> cursor(pt->bucket_start.begin(), pt->bucket_start.end() - 1);
-  pt->entries.assign(2 * std::max<size_t>(r, 1), 0);
-  for (size_t i = 0; i < r; ++i) {
-    const uint32_t e = cursor[keys[i] & (nb - 1)]++;
-    pt->entries[2 * e] = keys[i];
-    pt->entries[2 * e + 1] = static_cast<uint32_t>(i);
+  pt->entries.assign(2 * std::max<size_t>(ents.size(), 1), 0);
+  for (const Ent& e : ents) {
+    const uint32_t x = cursor[e.key & (nb - 1)]++;
+    pt->entries[2 * x] = e.key;
+    pt->entries[2 * x + 1] = e.tag;
   }
 }
 

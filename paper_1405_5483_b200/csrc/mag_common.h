@@ -102,6 +102,12 @@ struct ScanPlan {
   uint64_t match_mask;
   // verification
   uint32_t m, maxlen, key_len;
+  // Window keys (strided plans, q > 1): the pattern table indexes every
+  // (pattern, shift s < q) by the wkey_len bytes p[s, s + wkey_len); a
+  // candidate window is checked with ONE key read at its gram boundary q*ss,
+  // each hit naming the start q*ss - s directly.
+  int window_key;
+  uint32_t wkey_len;
   uint32_t pf_bits;       // prefilter bitmap has 2^pf_bits bits (smem)
   uint32_t bucket_bits;   // 2^bucket_bits buckets (global)
   uint32_t r;

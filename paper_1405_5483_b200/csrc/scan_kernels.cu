@@ -113,8 +113,12 @@ struct Smem {
   uint64_t* bars;     // [warp][ring]
 };
 
-template <int GM, typename E, bool TSMEM, int QW>
+// CMP / CK: compile-time m' and k (0 = read from the plan at run time).
+template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK>
 struct Scanner {
+  static constexpr int kEL = (CMP && CK) ? (CMP * CK <= 1 ? 0 : CMP * CK <= 2 ? 1 : CMP * CK <= 4 ? 2
+                                                             : CMP * CK <= 8 ? 3 : CMP * CK <= 16 ? 4 : -1)
+                                         : -1;  // entry log2 when known
   const ScanArgs& A;
   const Smem& S;
   const int lane, warp;
@@ -249,7 +253,7 @@ struct Scanner {
 
   // ----------------------------------------------------------- stage 1+2
   __device__ __forceinline__ E table_entry(uint32_t idx) const {
-    const uint32_t el = A.plan.entry_log2;
+    const uint32_t el = kEL >= 0 ? static_cast<uint32_t>(kEL) : A.plan.entry_log2;
     if constexpr (sizeof(E) == 8) {
       const uint64_t* t = TSMEM ? static_cast<const uint64_t*>(S.table)
                                 : static_cast<const uint64_t*>(A.table);
@@ -289,9 +293,8 @@ struct Scanner {
   }
 
   // ----------------------------------------------------------- stage 3
-  __device__ __forceinline__ uint32_t key_at(uint32_t r) const {
+  __device__ __forceinline__ uint32_t key_at(uint32_t r, uint32_t v) const {
     const uint32_t wi = r >> 2, sh = (r & 3u) << 3;
-    const uint32_t v = A.plan.key_len;
     const uint32_t w0 = sw[wi], w1 = sw[wi + 1];
     const uint32_t x0 = __funnelshift_r(w0, w1, sh) & key_word_mask(v, 0);
     uint32_t x1 = 0, x2 = 0, x3 = 0;
@@ -309,6 +312,7 @@ struct Scanner {
 
   __device__ __forceinline__ bool prefilter_pass(uint32_t key) const {
     const uint32_t pb = A.plan.pf_bits;
+    if (pb == 0) return true;
     const uint32_t i1 = key >> (32 - pb);
     const uint32_t i2 = ((key ^ (key >> 15)) * 0x2C1B3C6Du) >> (32 - pb);
     return ((S.pf[i1 >> 5] >> (i1 & 31)) & (S.pf[i2 >> 5] >> (i2 & 31)) & 1u) != 0;
@@ -365,7 +369,7 @@ struct Scanner {
     uint32_t key = 0, c = 0;
     const uint32_t r = static_cast<uint32_t>(a - static_cast<long long>(src));
     if (act) {
-      key = key_at(r);
+      key = key_at(r, A.plan.key_len);
       if (prefilter_pass(key)) c = probe(r, key, nullptr, 0);
     }
     if (!__any_sync(kFull, c != 0)) return;
@@ -375,10 +379,63 @@ struct Scanner {
     fill += total;
   }
 
+  // Window keys: the key at slot offset r0 (= gram boundary q*ss) against
+  // the (pattern, shift) index; entry shift s names start r0 - s.  Entries
+  // come in (shift descending, pattern ascending) order = text order.
+  __device__ uint32_t probe_window(uint32_t r0, uint32_t key, uint64_t* dst, uint32_t idx) const {
+    const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
+    const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
+    uint32_t c = 0;
+    for (uint32_t e = lo; e < hi; ++e) {
+      const uint2 ent = __ldg(A.bucket_entries + e);
+      if (ent.x != key) continue;
+      const uint32_t s = ent.y >> kPidBits, pid = ent.y & ((1u << kPidBits) - 1u);
+      if (s > r0 + src) continue;  // start before the text
+      const uint32_t r = r0 - s;
+      const unsigned long long a = src + r;
+      const uint32_t len = __ldg(A.pat_len + pid);
+      if (a + len > A.n || !equal_at(r, pid, len)) continue;
+      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, pid);
+      ++c;
+    }
+    return c;
+  }
+
+  // One candidate window per lane, in queue (= text) order.
+  __device__ void drain_windows(uint32_t qlen, long long ss_ref) {
+    __syncwarp();
+    const uint32_t q = A.plan.q, v = A.plan.wkey_len;
+    // slot offset of the gram boundary q*ss of queue entry 0
+    const long long base0 = ss_ref * static_cast<long long>(q) - static_cast<long long>(src);
+    const long long lim = static_cast<long long>(A.n) - static_cast<long long>(src) - v;  // key must fit
+    for (uint32_t i0 = 0; i0 < qlen; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      uint32_t key = 0, c = 0, r0 = 0;
+      if (i < qlen) {
+        const long long rr = base0 + static_cast<long long>(queue[i]) * q;
+        if (rr >= 0 && rr <= lim) {
+          r0 = static_cast<uint32_t>(rr);
+          key = key_at(r0, v);
+          if (prefilter_pass(key)) c = probe_window(r0, key, nullptr, 0);
+        }
+      }
+      if (!__any_sync(kFull, c != 0)) continue;
+      const uint32_t excl = warp_excl_scan(c, lane);
+      const uint32_t total = __shfl_sync(kFull, excl + c, 31);
+      if (c) probe_window(r0, key, out, fill + excl);
+      fill += total;
+    }
+    __syncwarp();
+  }
+
   // Verify the queued windows: (window, start) pairs spread over the lanes
   // in order, so each lane checks one start.  Entries are super positions
   // relative to ss_ref.
   __device__ void drain(uint32_t qlen, long long ss_ref) {
+    if (A.plan.window_key) {
+      drain_windows(qlen, ss_ref);
+      return;
+    }
     __syncwarp();
     const uint32_t pairs = qlen * W;
     for (uint32_t p0 = 0; p0 < pairs; p0 += 32) {
@@ -410,10 +467,16 @@ struct Scanner {
       }
       return;
     }
+    const int mp = CMP ? CMP : this->mp;
+    const int ov = mp - 1;
+    const int k = CK ? CK : this->k;
+    const int lead = mp <= 16 ? ov : 0;
+    const int adv = 32 - lead;
+    const uint32_t inv_mp = CMP ? (65536u + CMP - 1) / CMP : this->inv_mp;
     // slot offset of the gram of relative sample 0, and per-sample stride
     const int g0 = static_cast<int>(
         (P.overlapping ? in.t0 : ((in.t0 + 1) * P.k - 1) * P.q) - src);
-    const int gstep = static_cast<int>(qk);
+    const int gstep = CK ? (P.overlapping ? 1 : static_cast<int>(P.q) * CK) : static_cast<int>(qk);
     // super positions: ss = ss_ref + rel, rel = tr * k + (k - 1 - j) >= 0
     const long long ss_ref = (static_cast<long long>(in.t0) - ov) * k;
     // samples before the text start have no gram; samples < m'-1 never hit
@@ -518,7 +581,7 @@ struct Scanner {
   }
 };
 
-template <int GM, typename E, bool TSMEM, int QW>
+template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
@@ -549,7 +612,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
   }
-  Scanner<GM, E, TSMEM, QW> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
+  Scanner<GM, E, TSMEM, QW, CMP, CK> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
   sc.run();
 }
 
@@ -627,9 +690,9 @@ __global__ void mag_encode_kernel(const ScanPlan P, const uint8_t* __restrict__ 
   }
 }
 
-template <int GM, typename E, bool TSMEM, int QW>
+template <int GM, typename E, bool TSMEM, int QW, int CMP = 0, int CK = 0>
 cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
-  auto k = mag_scan_kernel<GM, E, TSMEM, QW>;
+  auto k = mag_scan_kernel<GM, E, TSMEM, QW, CMP, CK>;
   static int configured_smem = -1;  // per instantiation
   if (configured_smem != static_cast<int>(smem)) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -642,14 +705,27 @@ cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) 
   return cudaGetLastError();
 }
 
+// Hashed plans with (m', k) in {(1,1), (2,1), (1,2)} get fully specialised
+// inner loops; everything else runs the generic (run-time m', k) loop.
+template <int GM, typename E, bool TSMEM, int QW>
+cudaError_t launch_mk(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
+  if constexpr (sizeof(E) == 4) {
+    const uint32_t mp = a.plan.m_prime, k = a.plan.k;
+    if (mp == 1 && k == 1) return launch_t<GM, E, TSMEM, QW, 1, 1>(a, st, grid, smem);
+    if (mp == 2 && k == 1) return launch_t<GM, E, TSMEM, QW, 2, 1>(a, st, grid, smem);
+    if (mp == 1 && k == 2) return launch_t<GM, E, TSMEM, QW, 1, 2>(a, st, grid, smem);
+  }
+  return launch_t<GM, E, TSMEM, QW>(a, st, grid, smem);
+}
+
 template <int GM, typename E, bool TSMEM>
 cudaError_t launch_qw(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
   if constexpr (GM == kKHashed) {
     switch ((a.plan.q + 3) / 4) {
-      case 1: return launch_t<GM, E, TSMEM, 1>(a, st, grid, smem);
-      case 2: return launch_t<GM, E, TSMEM, 2>(a, st, grid, smem);
-      case 3: return launch_t<GM, E, TSMEM, 3>(a, st, grid, smem);
-      default: return launch_t<GM, E, TSMEM, 4>(a, st, grid, smem);
+      case 1: return launch_mk<GM, E, TSMEM, 1>(a, st, grid, smem);
+      case 2: return launch_mk<GM, E, TSMEM, 2>(a, st, grid, smem);
+      case 3: return launch_mk<GM, E, TSMEM, 3>(a, st, grid, smem);
+      default: return launch_mk<GM, E, TSMEM, 4>(a, st, grid, smem);
     }
   } else {
     return launch_t<GM, E, TSMEM, 1>(a, st, grid, smem);

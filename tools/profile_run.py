@@ -26,6 +26,9 @@ e = mag.Engine(w.patterns, **kw)
 d = torch.from_numpy(w.text).cuda()
 p = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
 s = torch.cuda.Stream()
+for _ in range(2):  # warm-up: lazy module load, workspace allocation
+    e.search_prepared_async(p, s.cuda_stream).close()
+torch.cuda.synchronize()
 mag.scan_timer(True)
 for _ in range(a.iters):
     e.search_prepared_async(p, s.cuda_stream).close()
