@@ -306,6 +306,7 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.chunk_samples = P.chunk_samples;
     a.back = P.back;
     a.slot_bytes = P.slot_bytes;
+    a.full_bytes = P.full_bytes;
     a.ring = P.ring;
     a.nwarps = P.nwarps;
     a.num_slices = g.num_slices;

@@ -250,29 +250,37 @@ double key_hits(double keys, double sigma, unsigned v) {
   return universe > 1e15 ? 0.0 : keys / universe;
 }
 
+uint32_t gcd32(uint32_t a, uint32_t b) {
+  while (b) {
+    const uint32_t t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
 // Chunk / slice / slot sizes of the warp-streaming kernel.
 void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
   const ScanPlan& sp = P->sp;
   const uint32_t ov = sp.m_prime ? sp.m_prime - 1 : 0;
-  const uint32_t adv = sp.verify_all ? 32 : (sp.m_prime <= 16 ? 32 - ov : 32);
-  const uint32_t bytes_per_sample = sp.verify_all || sp.overlapping ? 1 : sp.q * sp.k;
+  const uint32_t bps = sp.verify_all || sp.overlapping ? 1 : sp.q * sp.k;  // bytes per sample
   const uint32_t target = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes) : kChunkTarget;
-  const uint32_t iters = std::max<uint32_t>(1, (target + adv * bytes_per_sample / 2) / (adv * bytes_per_sample));
-  P->chunk_samples = iters * adv;
-  const uint64_t chunk_bytes = static_cast<uint64_t>(P->chunk_samples) * bytes_per_sample;
-  P->slice_samples = static_cast<uint64_t>(P->chunk_samples) *
+  // interior chunks advance by a multiple of 16 bytes (aligned TMA windows)
+  const uint32_t m16 = 16 / gcd32(16, bps);
+  uint32_t c = std::max<uint32_t>(32, target / bps / m16 * m16);
+  c = (c + m16 - 1) / m16 * m16;
+  P->chunk_samples = c;
+  const uint64_t chunk_bytes = static_cast<uint64_t>(c) * bps;
+  P->slice_samples = static_cast<uint64_t>(c) *
                      std::max<uint64_t>(1, (kSliceTarget + chunk_bytes / 2) / chunk_bytes);
   // pattern reach after the last gram: full patterns up to 1 KiB stay in the
   // slot, longer ones are compared from global memory; >= 16 + 4 key bytes
   P->back = static_cast<uint32_t>(std::min<uint64_t>(pd.maxlen, 1024) + 24);
-  uint64_t window;
-  if (sp.verify_all)
-    window = P->chunk_samples;
-  else if (sp.overlapping)
-    window = static_cast<uint64_t>(P->chunk_samples) + ov + sp.q;
-  else
-    window = (static_cast<uint64_t>(P->chunk_samples) + ov) * sp.q * sp.k + sp.q;
-  P->slot_bytes = static_cast<uint32_t>(align16(window + P->back + 15 + 32));
+  const uint64_t qm1 = sp.overlapping || sp.verify_all ? 0 : sp.q - 1;
+  const uint64_t extra = sp.overlapping ? sp.q : 0;
+  P->full_bytes = static_cast<uint32_t>(
+      align16(chunk_bytes + static_cast<uint64_t>(ov) * bps + qm1 + extra + P->back + 15));
+  P->slot_bytes = P->full_bytes + 32;
   P->ring = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultRing;
   P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kDefaultWarps;
 }

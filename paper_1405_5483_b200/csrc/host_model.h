@@ -85,6 +85,7 @@ struct Plan {
   uint32_t chunk_samples = 0;  // samples per ring slot
   uint64_t slice_samples = 0;  // samples per warp work item
   uint32_t back = 0;           // staged bytes after a chunk's last gram
+  uint32_t full_bytes = 0;     // staged bytes of an interior chunk
   uint32_t slot_bytes = 0;
   uint32_t ring = 0, nwarps = 0;
   double pred_cand_per_byte = 0;

@@ -122,10 +122,12 @@ constexpr int kQueueCap = 64;   // candidate windows queued per warp
 // Per ring slot: what the staged bytes are.
 struct SlotInfo {
   unsigned long long slice;     // owning slice
-  unsigned long long t0, t1;    // samples [t0, t1) of this chunk
+  unsigned long long t0;        // first sample of this chunk
   unsigned long long src;       // absolute offset of slot byte 0
-  unsigned int first, last;     // first / last chunk of its slice
-  unsigned int valid, pad;      // staged bytes
+  unsigned int nsamp;           // samples [t0, t0 + nsamp)
+  unsigned int valid;           // staged bytes
+  unsigned int flags;           // 1: first chunk of its slice, 2: last chunk
+  unsigned int pad;
 };
 
 MAG_HD size_t align16(size_t x) { return (x + 15) & ~size_t(15); }

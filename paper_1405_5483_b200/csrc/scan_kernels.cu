@@ -114,7 +114,8 @@ struct Smem {
 };
 
 // CMP / CK: compile-time m' and k (0 = read from the plan at run time).
-template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK>
+// A4: hashed grams start on 4-byte boundaries (q*k and q multiples of 4).
+template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK, bool A4>
 struct Scanner {
   static constexpr int kEL = (CMP && CK) ? (CMP * CK <= 1 ? 0 : CMP * CK <= 2 ? 1 : CMP * CK <= 4 ? 2
                                                              : CMP * CK <= 8 ? 3 : CMP * CK <= 16 ? 4 : -1)
@@ -172,35 +173,19 @@ struct Scanner {
   }
 
   // ------------------------------------------------------------- loader
-  // Bytes a chunk of samples [t0, t1) needs: the grams of its samples (and
-  // of the m'-1 samples before), the candidate windows they can raise (up
-  // to q*k*ov + q - 1 bytes before its first gram) and the pattern reach.
-  __device__ __forceinline__ void chunk_window(unsigned long long t0, unsigned long long t1,
-                                               unsigned long long* lo, unsigned long long* hi) const {
+  // A chunk of samples [t0, t1) stages text [lo, hi): the grams of its
+  // samples (and of the m'-1 samples before), every candidate window they
+  // can raise (starting up to q*k*ov + q - 1 bytes before the first gram)
+  // and the pattern reach after the last gram.  lo is 16-byte aligned;
+  // interior chunks stage exactly full_bytes.
+  __device__ __forceinline__ long long raw_lo(unsigned long long t0) const {
     const ScanPlan& P = A.plan;
-    const long long ov = static_cast<long long>(P.m_prime) - 1;
-    long long l, h;
-    if (P.verify_all) {
-      l = static_cast<long long>(t0);
-      h = static_cast<long long>(t1) + A.back;
-    } else if (P.overlapping) {
-      l = static_cast<long long>(t0) - ov;
-      h = static_cast<long long>(t1) + P.q + A.back;
-    } else {
-      const long long qk = static_cast<long long>(P.q) * P.k;
-      l = (static_cast<long long>(t0) - ov) * qk - (static_cast<long long>(P.q) - 1);
-      h = static_cast<long long>(t1) * qk + A.back;
-    }
-    if (l < 0) l = 0;
-    l &= ~15ll;
-    if (h > static_cast<long long>(A.n)) h = static_cast<long long>(A.n);
-    if (h < l) h = l;
-    *lo = static_cast<unsigned long long>(l);
-    *hi = static_cast<unsigned long long>(h);
+    const long long qm1 = (P.overlapping || P.verify_all) ? 0 : static_cast<long long>(P.q) - 1;
+    return (static_cast<long long>(t0) - ov) * static_cast<long long>(qk) - qm1;
   }
 
-  // Issue the next chunk of this warp's stream into slot loads % ring.
-  // Returns false when the warp has no more work.  Warp-uniform.
+  // Issue the next chunk of this warp's stream into slot lslot.  Returns
+  // false when the warp has no more work.  Warp-uniform.
   __device__ bool issue() {
     while (!ld_done && ld_t >= ld_tend) {
       unsigned long long x = 0;
@@ -218,17 +203,27 @@ struct Scanner {
     }
     if (ld_done) return false;
     const unsigned long long t0 = ld_t;
-    unsigned long long t1 = t0 + A.chunk_samples;
-    if (t1 > ld_tend) t1 = ld_tend;
-    unsigned long long lo, hi;
-    chunk_window(t0, t1, &lo, &hi);
+    const unsigned long long left = ld_tend - t0;
+    const uint32_t nsamp = left < A.chunk_samples ? static_cast<uint32_t>(left) : A.chunk_samples;
+    const long long rl = raw_lo(t0);
+    unsigned long long lo = rl > 0 ? static_cast<unsigned long long>(rl) & ~15ull : 0ull;
+    uint32_t bulk, len;
+    if (nsamp == A.chunk_samples && rl >= 0 && lo + A.full_bytes <= A.n) {
+      bulk = len = A.full_bytes;  // interior chunk
+    } else {
+      const ScanPlan& P = A.plan;
+      const unsigned long long extra = P.overlapping ? P.q : 0;
+      unsigned long long hi = (t0 + nsamp) * qk + extra + A.back;
+      if (hi > A.n) hi = A.n;
+      if (hi < lo) hi = lo;
+      // whole 16-byte blocks except at the very end of the text
+      const unsigned long long hi16 = (hi + 15) & ~15ull;
+      const unsigned long long bulk_end = hi16 <= A.n ? hi16 : (A.n & ~15ull);
+      bulk = bulk_end > lo ? static_cast<uint32_t>(bulk_end - lo) : 0u;
+      len = static_cast<uint32_t>(hi - lo) > bulk ? static_cast<uint32_t>(hi - lo) : bulk;
+    }
     const uint32_t slot = lslot;
     lslot = lslot + 1 == A.ring ? 0 : lslot + 1;
-    // whole 16-byte blocks except at the very end of the text
-    const unsigned long long hi16 = (hi + 15) & ~15ull;
-    const unsigned long long bulk_end = hi16 <= A.n ? hi16 : (A.n & ~15ull);
-    const uint32_t bulk = bulk_end > lo ? static_cast<uint32_t>(bulk_end - lo) : 0u;
-    const uint32_t len = static_cast<uint32_t>(hi - lo) > bulk ? static_cast<uint32_t>(hi - lo) : bulk;
     uint8_t* dst = myslots + static_cast<size_t>(slot) * A.slot_bytes;
     if (static_cast<uint32_t>(lane) < len - bulk) dst[bulk + lane] = __ldg(A.text + lo + bulk + lane);
     __syncwarp();
@@ -236,17 +231,16 @@ struct Scanner {
       SlotInfo& in = myinfo[slot];
       in.slice = ld_slice;
       in.t0 = t0;
-      in.t1 = t1;
       in.src = lo;
-      in.first = t0 == ld_slice * A.slice_samples;
-      in.last = t1 == ld_tend;
+      in.nsamp = nsamp;
       in.valid = len;
+      in.flags = (t0 == ld_slice * A.slice_samples ? 1u : 0u) | (t0 + nsamp == ld_tend ? 2u : 0u);
       fence_proxy_async();
       mbar_arrive_expect_tx(mybars + slot, bulk);
       if (bulk) tma_load_1d(dst, A.text + lo, bulk, mybars + slot);
     }
     __syncwarp();
-    ld_t = t1;
+    ld_t = t0 + nsamp;
     ++loads;
     return true;
   }
@@ -274,13 +268,27 @@ struct Scanner {
       const unsigned long long u = P.overlapping ? t : (t + 1) * P.k - 1;
       return table_entry(__ldg(A.codes + u));
     } else if constexpr (GM == kKHashed) {
-      const uint32_t wi = rel >> 2, sh = (rel & 3u) << 3;
-      uint32_t w[QW + 1];
-#pragma unroll
-      for (int i = 0; i <= QW; ++i) w[i] = sw[wi + i];
+      const uint32_t wi = rel >> 2;
       uint32_t x[4] = {0, 0, 0, 0};
+      if constexpr (A4) {
+        if constexpr (QW == 4) {
+          const uint4 v = *reinterpret_cast<const uint4*>(sw + wi);  // 16-byte aligned grams
+          x[0] = v.x;
+          x[1] = v.y;
+          x[2] = v.z;
+          x[3] = v.w;
+        } else {
 #pragma unroll
-      for (int i = 0; i < QW; ++i) x[i] = __funnelshift_r(w[i], w[i + 1], sh);
+          for (int i = 0; i < QW; ++i) x[i] = sw[wi + i];
+        }
+      } else {
+        const uint32_t sh = (rel & 3u) << 3;
+        uint32_t w[QW + 1];
+#pragma unroll
+        for (int i = 0; i <= QW; ++i) w[i] = sw[wi + i];
+#pragma unroll
+        for (int i = 0; i < QW; ++i) x[i] = __funnelshift_r(w[i], w[i + 1], sh);
+      }
       const uint32_t rem = P.q - 4u * (QW - 1);  // 1..4 bytes in the last word
       x[QW - 1] &= rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
       return table_entry(hash_gram_words(x[0], x[1], x[2], x[3]) >> (32 - P.table_bits));
@@ -455,9 +463,60 @@ struct Scanner {
   }
 
   // ------------------------------------------------------------ a chunk
+  // Queue the candidates of a sub-iteration (lane order = sample order).
+  __device__ __forceinline__ void enqueue(E hits, int tr, int k, uint32_t inv_mp, uint32_t& qlen,
+                                          long long ss_ref) {
+    const unsigned hb = __ballot_sync(kFull, hits != 0);
+    if (!hb) return;
+    if (k == 1) {
+      // one alignment: at most one candidate per lane
+      const uint32_t total = __popc(hb);
+      cands += hits ? 1u : 0u;
+      if (qlen + total > kQueueCap) {
+        drain(qlen, ss_ref);
+        qlen = 0;
+      }
+      if (hits) queue[qlen + __popc(hb & ((1u << lane) - 1u))] = static_cast<uint32_t>(tr);
+      __syncwarp();
+      qlen += total;
+      return;
+    }
+    // k alignments: a lane's candidates in ascending super position
+    // (alignment j descending): rel = tr * k + (k - 1 - j)
+    const uint32_t cnt = popc_e(hits);
+    cands += cnt;
+    const uint32_t excl = warp_excl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
+    const int rel_base = tr * k + (k - 1);
+    uint32_t done = 0;
+    while (done < total) {
+      if (qlen == kQueueCap) {
+        drain(qlen, ss_ref);
+        qlen = 0;
+      }
+      const uint32_t take = min(static_cast<uint32_t>(kQueueCap) - qlen, total - done);
+      if (cnt) {
+        uint32_t rank = excl;
+        E h = hits;
+        while (h) {
+          const int bit = top_bit(h);
+          h &= static_cast<E>(~(E(1) << bit));
+          if (rank >= done && rank < done + take) {
+            const int j = static_cast<int>((static_cast<uint32_t>(bit) * inv_mp) >> 16);
+            queue[qlen + rank - done] = static_cast<uint32_t>(rel_base - j);
+          }
+          ++rank;
+        }
+      }
+      __syncwarp();
+      qlen += take;
+      done += take;
+    }
+  }
+
   __device__ void process_chunk(const SlotInfo& in) {
     const ScanPlan& P = A.plan;
-    const int nsamp = static_cast<int>(in.t1 - in.t0);
+    const int nsamp = static_cast<int>(in.nsamp);
     if (P.verify_all) {
       // every start is a candidate: one start per lane, in order
       const long long t0 = static_cast<long long>(in.t0);
@@ -470,8 +529,6 @@ struct Scanner {
     const int mp = CMP ? CMP : this->mp;
     const int ov = mp - 1;
     const int k = CK ? CK : this->k;
-    const int lead = mp <= 16 ? ov : 0;
-    const int adv = 32 - lead;
     const uint32_t inv_mp = CMP ? (65536u + CMP - 1) / CMP : this->inv_mp;
     // slot offset of the gram of relative sample 0, and per-sample stride
     const int g0 = static_cast<int>(
@@ -485,67 +542,44 @@ struct Scanner {
     const E mm = static_cast<E>(P.match_mask);
     const E ones = static_cast<E>(~E(0));
     uint32_t qlen = 0;
-    for (int base = -lead; base + lead < nsamp; base += adv) {
-      const int tr = base + lane;
-      E D;
-      if (mp <= 16) {
-        const E M = (tr >= tmin && tr < nsamp) ? gram_mask(static_cast<uint32_t>(g0 + tr * gstep), in.t0 + tr) : ones;
-        D = M;
-        for (int i = 1; i <= ov; ++i) D |= static_cast<E>(shfl_up_e(M, i) << i);
-      } else {
-        D = static_cast<E>(0);
+    if (mp <= 16) {
+      // two samples per lane per step (tr and tr + 32): independent gram
+      // chains for the scheduler; D needs the m'-1 previous samples' masks
+      const int lead = ov;
+      for (int base = -lead; base + lead < nsamp; base += 64 - lead) {
+        const int ta = base + lane, tb = ta + 32;
+        const bool va = ta >= tmin && ta < nsamp, vb = tb < nsamp;
+        // divergence-free: invalid lanes read a safe slot offset
+        const E ma = gram_mask(static_cast<uint32_t>(va ? g0 + ta * gstep : 0), in.t0 + (va ? ta : 0));
+        const E mb = gram_mask(static_cast<uint32_t>(vb ? g0 + tb * gstep : 0), in.t0 + (vb ? tb : 0));
+        const E Ma = va ? ma : ones, Mb = vb ? mb : ones;
+        E Da = Ma, Db = Mb;
+#pragma unroll
+        for (int i = 1; i <= (CMP ? CMP - 1 : 15); ++i) {
+          if (!CMP && i > ov) break;
+          const E ua = shfl_up_e(Ma, i);
+          const E ub = shfl_up_e(Mb, i);
+          const E wa = __shfl_sync(kFull, Ma, (lane - i) & 31);  // b's predecessors in a
+          Da |= static_cast<E>(ua << i);
+          Db |= static_cast<E>((lane >= i ? ub : wa) << i);
+        }
+        const E ha = (lane >= lead && ta >= thit && ta < nsamp) ? static_cast<E>(~Da & mm) : static_cast<E>(0);
+        const E hb = (tb >= thit && tb < nsamp) ? static_cast<E>(~Db & mm) : static_cast<E>(0);
+        enqueue(ha, ta, k, inv_mp, qlen, ss_ref);
+        enqueue(hb, tb, k, inv_mp, qlen, ss_ref);
+      }
+    } else {
+      for (int base = 0; base < nsamp; base += 32) {
+        const int tr = base + lane;
+        E D = static_cast<E>(0);
         for (int i = 0; i < mp; ++i) {
           const int ti = tr - i;
-          const E M = (ti >= tmin && ti < nsamp) ? gram_mask(static_cast<uint32_t>(g0 + ti * gstep), in.t0 + ti) : ones;
-          D |= static_cast<E>(M << i);
+          const bool v = ti >= tmin && ti < nsamp;
+          const E M = gram_mask(static_cast<uint32_t>(v ? g0 + ti * gstep : 0), in.t0 + (v ? ti : 0));
+          D |= static_cast<E>((v ? M : ones) << i);
         }
-      }
-      const E hits = (lane >= lead && tr >= thit && tr < nsamp) ? static_cast<E>(~D & mm) : static_cast<E>(0);
-      const unsigned hb = __ballot_sync(kFull, hits != 0);
-      if (!hb) continue;
-      if (k == 1) {
-        // one alignment: at most one candidate per lane, ballot order
-        const uint32_t total = __popc(hb);
-        cands += hits ? 1u : 0u;
-        if (qlen + total > kQueueCap) {
-          drain(qlen, ss_ref);
-          qlen = 0;
-        }
-        if (hits) queue[qlen + __popc(hb & ((1u << lane) - 1u))] = static_cast<uint32_t>(tr);
-        __syncwarp();
-        qlen += total;
-        continue;
-      }
-      // k alignments: candidates of a lane in ascending super position
-      // (alignment j descending)
-      const uint32_t cnt = popc_e(hits);
-      cands += cnt;
-      const uint32_t excl = warp_excl_scan(cnt, lane);
-      const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
-      const int rel_base = tr * k + (k - 1);
-      uint32_t done = 0;
-      while (done < total) {
-        if (qlen == kQueueCap) {
-          drain(qlen, ss_ref);
-          qlen = 0;
-        }
-        const uint32_t take = min(static_cast<uint32_t>(kQueueCap) - qlen, total - done);
-        if (cnt) {
-          uint32_t rank = excl;
-          E h = hits;
-          while (h) {
-            const int bit = top_bit(h);
-            h &= static_cast<E>(~(E(1) << bit));
-            if (rank >= done && rank < done + take) {
-              const int j = static_cast<int>((static_cast<uint32_t>(bit) * inv_mp) >> 16);
-              queue[qlen + rank - done] = static_cast<uint32_t>(rel_base - j);
-            }
-            ++rank;
-          }
-        }
-        __syncwarp();
-        qlen += take;
-        done += take;
+        const E hits = (tr >= thit && tr < nsamp) ? static_cast<E>(~D & mm) : static_cast<E>(0);
+        enqueue(hits, tr, k, inv_mp, qlen, ss_ref);
       }
     }
     if (qlen) drain(qlen, ss_ref);
@@ -566,10 +600,10 @@ struct Scanner {
       sw = reinterpret_cast<const uint32_t*>(sb);
       src = in.src;
       valid = in.valid;
-      if (in.first) fill = 0;
+      if (in.flags & 1u) fill = 0;
       out = A.staging + static_cast<size_t>(in.slice) * A.slice_cap;
       process_chunk(in);
-      if (in.last && lane == 0) A.slice_count[in.slice] = fill;
+      if ((in.flags & 2u) && lane == 0) A.slice_count[in.slice] = fill;
       __syncwarp();
       ++cons;
       issue();
@@ -581,7 +615,7 @@ struct Scanner {
   }
 };
 
-template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK>
+template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK, bool A4>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
@@ -612,7 +646,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
   }
-  Scanner<GM, E, TSMEM, QW, CMP, CK> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
+  Scanner<GM, E, TSMEM, QW, CMP, CK, A4> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
   sc.run();
 }
 
@@ -690,9 +724,9 @@ __global__ void mag_encode_kernel(const ScanPlan P, const uint8_t* __restrict__ 
   }
 }
 
-template <int GM, typename E, bool TSMEM, int QW, int CMP = 0, int CK = 0>
+template <int GM, typename E, bool TSMEM, int QW, int CMP = 0, int CK = 0, bool A4 = false>
 cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
-  auto k = mag_scan_kernel<GM, E, TSMEM, QW, CMP, CK>;
+  auto k = mag_scan_kernel<GM, E, TSMEM, QW, CMP, CK, A4>;
   static int configured_smem = -1;  // per instantiation
   if (configured_smem != static_cast<int>(smem)) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -707,25 +741,34 @@ cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) 
 
 // Hashed plans with (m', k) in {(1,1), (2,1), (1,2)} get fully specialised
 // inner loops; everything else runs the generic (run-time m', k) loop.
-template <int GM, typename E, bool TSMEM, int QW>
+template <int GM, typename E, bool TSMEM, int QW, bool A4>
 cudaError_t launch_mk(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
   if constexpr (sizeof(E) == 4) {
     const uint32_t mp = a.plan.m_prime, k = a.plan.k;
-    if (mp == 1 && k == 1) return launch_t<GM, E, TSMEM, QW, 1, 1>(a, st, grid, smem);
-    if (mp == 2 && k == 1) return launch_t<GM, E, TSMEM, QW, 2, 1>(a, st, grid, smem);
-    if (mp == 1 && k == 2) return launch_t<GM, E, TSMEM, QW, 1, 2>(a, st, grid, smem);
+    if (mp == 1 && k == 1) return launch_t<GM, E, TSMEM, QW, 1, 1, A4>(a, st, grid, smem);
+    if (mp == 2 && k == 1) return launch_t<GM, E, TSMEM, QW, 2, 1, A4>(a, st, grid, smem);
+    if (mp == 1 && k == 2) return launch_t<GM, E, TSMEM, QW, 1, 2, A4>(a, st, grid, smem);
   }
-  return launch_t<GM, E, TSMEM, QW>(a, st, grid, smem);
+  return launch_t<GM, E, TSMEM, QW, 0, 0, A4>(a, st, grid, smem);
+}
+
+template <int GM, typename E, bool TSMEM, int QW>
+cudaError_t launch_a4(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
+  // grams start on 4-byte boundaries when q and the sample stride are
+  // multiples of 4 (strided only; slot bases are 16-byte aligned)
+  const bool a4 = !a.plan.overlapping && a.plan.q % 4 == 0;
+  if (a4) return launch_mk<GM, E, TSMEM, QW, true>(a, st, grid, smem);
+  return launch_mk<GM, E, TSMEM, QW, false>(a, st, grid, smem);
 }
 
 template <int GM, typename E, bool TSMEM>
 cudaError_t launch_qw(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) {
   if constexpr (GM == kKHashed) {
     switch ((a.plan.q + 3) / 4) {
-      case 1: return launch_mk<GM, E, TSMEM, 1>(a, st, grid, smem);
-      case 2: return launch_mk<GM, E, TSMEM, 2>(a, st, grid, smem);
-      case 3: return launch_mk<GM, E, TSMEM, 3>(a, st, grid, smem);
-      default: return launch_mk<GM, E, TSMEM, 4>(a, st, grid, smem);
+      case 1: return launch_a4<GM, E, TSMEM, 1>(a, st, grid, smem);
+      case 2: return launch_a4<GM, E, TSMEM, 2>(a, st, grid, smem);
+      case 3: return launch_a4<GM, E, TSMEM, 3>(a, st, grid, smem);
+      default: return launch_a4<GM, E, TSMEM, 4>(a, st, grid, smem);
     }
   } else {
     return launch_t<GM, E, TSMEM, 1>(a, st, grid, smem);

@@ -32,7 +32,8 @@ struct ScanArgs {
   uint64_t slice_samples;       // multiple of chunk_samples
   uint32_t chunk_samples;       // samples per chunk (iterations * advance)
   uint32_t back;                // staged bytes after the last gram (pattern reach)
-  uint32_t slot_bytes;          // one ring slot (multiple of 16)
+  uint32_t full_bytes;          // staged bytes of an interior chunk (multiple of 16)
+  uint32_t slot_bytes;          // one ring slot (multiple of 16, >= full_bytes + 32)
   uint32_t ring;                // slots per warp
   uint32_t nwarps;              // warps per CTA
   uint64_t slice_begin, slice_end;  // slices of this launch
