@@ -241,7 +241,8 @@ double prefilter_fp(double keys, unsigned pf_bits) {
 // a queue slot, per verified start a rolled key + prefilter, per prefilter
 // pass an L2 bucket probe.
 constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 10, kCostStart = 45,
-                 kCostWindow = 45, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40;
+                 kCostWindow = 45, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40,
+                 kCostChunk = 4800;  // per staged chunk (loader + bookkeeping), thread-instr
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -264,7 +265,8 @@ void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
   const ScanPlan& sp = P->sp;
   const uint32_t ov = sp.m_prime ? sp.m_prime - 1 : 0;
   const uint32_t bps = sp.verify_all || sp.overlapping ? 1 : sp.q * sp.k;  // bytes per sample
-  const uint32_t target = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes) : kChunkTarget;
+  const uint32_t target = rq.tile_bytes > 0 ? static_cast<uint32_t>(rq.tile_bytes)
+                                            : (P->chunk_target ? P->chunk_target : kChunkTarget);
   // interior chunks advance by a multiple of 16 bytes (aligned TMA windows)
   const uint32_t m16 = 16 / gcd32(16, bps);
   uint32_t c = std::max<uint32_t>(32, target / bps / m16 * m16);
@@ -391,33 +393,47 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->mapping = kMapIdentity;
     for (int c = 0; c < 256; ++c) P->map[c] = static_cast<uint8_t>(c);
     sp.sigma_prime = 256;
-    // shared memory left for table + prefilter once the warp rings are in
-    auto room_for = [&](unsigned q, unsigned k, unsigned mp, int va) {
+    // shared memory left for table + prefilter once the warp rings (of a
+    // given chunk size) are in
+    auto room_for = [&](unsigned q, unsigned k, unsigned mp, int va, uint32_t chunk) {
       Plan probe = *P;
       probe.sp.q = q;
       probe.sp.k = k;
       probe.sp.m_prime = mp;
       probe.sp.verify_all = va;
+      probe.chunk_target = chunk;
       finish_geometry(pd, rq, &probe);
       const size_t f = fixed_smem(probe) + 1024;
       return rq.smem_limit > f ? rq.smem_limit - f : size_t(0);
     };
+    static const uint32_t kChunks[] = {4096, 3072, 2048, 1536, 1024, 768, 512};
+    static const unsigned kPf[] = {0, 16, 17, 18, 19, 20, 21};
     const double keys = static_cast<double>(pd.r);
     struct Cand {
       double cost = std::numeric_limits<double>::infinity();
-      unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 7;
+      unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 0;
+      uint32_t chunk = kChunkTarget;
       bool va = true;
       double cpb = 1;
     } best;
-    // verify-all baseline: whole room to the prefilter
-    {
-      const size_t room = room_for(1, 1, 1, 1);
-      unsigned pf = 7;
-      while (pf < 24 && (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
-      best.cost = kCostVerifyAll + prefilter_fp(keys, pf) * kCostProbe +
-                  key_hits(keys, sigma_obs, static_cast<unsigned>(std::min<size_t>(m, 16))) * kCostCompare;
-      best.pf = pf;
-      best.cpb = 1;
+    auto pf_bytes = [](unsigned pf) { return pf ? align16((size_t(1) << pf) / 8) : size_t(16); };
+    // verify-all baseline
+    for (unsigned pf : kPf) {
+      for (uint32_t chunk : kChunks) {
+        if (rq.tile_bytes > 0 && chunk != kChunks[0]) break;
+        if (pf_bytes(pf) > room_for(1, 1, 1, 1, chunk)) continue;
+        const double cost = kCostVerifyAll + kCostChunk / chunk +
+                            (pf ? prefilter_fp(keys, pf) : 1.0) * kCostProbe +
+                            key_hits(keys, sigma_obs, static_cast<unsigned>(std::min<size_t>(m, 16))) *
+                                kCostCompare;
+        if (cost < best.cost) {
+          best.cost = cost;
+          best.pf = pf;
+          best.chunk = chunk;
+          best.cpb = 1;
+        }
+        break;  // largest chunk that fits
+      }
     }
     if (rq.table_bits >= 0) {
       const unsigned qmax = sp.overlapping ? static_cast<unsigned>(std::min<size_t>(16, m))
@@ -432,43 +448,49 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           if (rq.k > 0 && !sp.overlapping && k != static_cast<unsigned>(rq.k)) continue;
           const unsigned mpmax = static_cast<unsigned>(std::min<size_t>(L / k, w / k));
           for (unsigned mp = 1; mp <= mpmax; ++mp) {
-            const size_t room = room_for(q, k, mp, 0);
             const unsigned el = pow2ceil_log2(std::max(1u, k * mp));
-            for (unsigned tbits = 14; tbits <= 24; ++tbits) {
-              const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
-              if (tbytes + 16 > room) break;
+            const double sample_cost = (kCostSample + (mp - 1) * kCostShift) /
+                                       (sp.overlapping ? 1.0 : static_cast<double>(k * q));
+            const bool wkey = !sp.overlapping && q > 1;
+            const double nkeys = wkey ? keys * q : keys;
+            const double hits = key_hits(nkeys, sigma_obs,
+                                         static_cast<unsigned>(wkey ? std::min<size_t>(16, m - q + 1)
+                                                                    : std::min<size_t>(16, m)));
+            for (unsigned tbits = 12; tbits <= 24; ++tbits) {
               if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
-              unsigned pf = 7;
-              while (pf < 24 && tbytes + (size_t(1) << (pf + 1)) / 8 <= room) ++pf;
+              const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
               const double adm = sp.overlapping ? keys : keys * q;
               const double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
               const double pm = std::pow(p, static_cast<double>(mp));
-              double cost, cpb;
-              if (sp.overlapping) {
-                cpb = pm;
-                cost = kCostSample + (mp - 1) * kCostShift +
-                       pm * (kCostCand + kCostStart + prefilter_fp(keys, pf) * kCostProbe);
-              } else {
-                cpb = pm / q;  // k alignments per sample, one sample per k*q bytes
-                if (q > 1)     // window keys: one probe per candidate, r*q keys indexed
-                  cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) +
-                         cpb * (kCostCand + kCostWindow + prefilter_fp(keys * q, pf) * kCostProbe +
-                                key_hits(keys * q, sigma_obs,
-                                         static_cast<unsigned>(std::min<size_t>(16, m - q + 1))) *
-                                    kCostCompare);
-                else
-                  cost = (kCostSample + (mp - 1) * kCostShift) / (k * q) + cpb * kCostCand +
-                         pm * (kCostStart + prefilter_fp(keys, pf) * kCostProbe);
-              }
-              if (cost < best.cost * 0.999) {
-                best.cost = cost;
-                best.q = q;
-                best.k = k;
-                best.mp = mp;
-                best.tb = tbits;
-                best.pf = pf;
-                best.va = false;
-                best.cpb = cpb;
+              // candidates per byte, and verified starts per byte
+              const double cpb = sp.overlapping ? pm : pm / q;
+              for (unsigned pf : kPf) {
+                uint32_t chunk = 0;
+                for (uint32_t c : kChunks) {
+                  if (rq.tile_bytes > 0 && c != kChunks[0]) break;
+                  if (tbytes + pf_bytes(pf) <= room_for(q, k, mp, 0, c)) {
+                    chunk = c;
+                    break;
+                  }
+                }
+                if (!chunk) continue;
+                const double fp = pf ? prefilter_fp(nkeys, pf) : 1.0;
+                double cost = sample_cost + kCostChunk / chunk;
+                if (wkey)  // window keys: one probe per candidate
+                  cost += cpb * (kCostCand + kCostWindow + fp * kCostProbe + hits * kCostCompare);
+                else       // start keys: one probe per verified start
+                  cost += cpb * kCostCand + pm * (kCostStart + fp * kCostProbe + hits * kCostCompare);
+                if (cost < best.cost * 0.999) {
+                  best.cost = cost;
+                  best.q = q;
+                  best.k = k;
+                  best.mp = mp;
+                  best.tb = tbits;
+                  best.pf = pf;
+                  best.chunk = chunk;
+                  best.va = false;
+                  best.cpb = cpb;
+                }
               }
             }
           }
@@ -490,6 +512,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.entries = 1ull << best.tb;
     }
     sp.pf_bits = best.pf;
+    P->chunk_target = best.chunk;
     P->pred_cand_per_byte = best.cpb;
   }
 

@@ -82,6 +82,7 @@ struct Plan {
   int mapping = 0;           // mag_mapping in effect
   uint8_t map[256] = {0};
   // kernel geometry (scan_launch.h ScanArgs)
+  uint32_t chunk_target = 0;   // planner's chunk size (gram bytes), 0 = default
   uint32_t chunk_samples = 0;  // samples per ring slot
   uint64_t slice_samples = 0;  // samples per warp work item
   uint32_t back = 0;           // staged bytes after a chunk's last gram
