@@ -57,6 +57,7 @@ typedef struct mag_plan_info {
   uint32_t tile_bytes, halo, warps, stages;
   size_t smem_bytes;
   double predicted_candidates_per_byte;
+  uint32_t probes;      /* hashed, m' = k = 1: table entries probed per gram */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

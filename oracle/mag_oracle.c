@@ -109,6 +109,19 @@ uint32_t mo_gram_hash(const uint8_t* p, unsigned q) {
   return h;
 }
 
+/* Multi-probe hashed grams (GPU extension; paper_1405_5483_b200/csrc/
+ * mag_common.h probe_block/probe_bit): `probes` entries inside one 32-entry
+ * block, admitted only where all of them are admitted. */
+static inline uint32_t probe_entry(const mo_params* P, uint32_t h, unsigned i) {
+  uint32_t blk = h >> (37 - P->table_bits);
+  uint32_t bit = ((h * 0x9E3779B1u) >> (27 - 5 * i)) & 31u;
+  return (blk << 5) | bit;
+}
+
+static inline int multi_probe(const mo_params* P) {
+  return P->gram_mode == MO_GRAM_HASHED && P->probes > 1;
+}
+
 static inline uint32_t gram_index(const mo_params* P, const uint8_t* g) {
   if (P->gram_mode == MO_GRAM_EXACT) return mo_encode_gram(P->map, P->sigma_prime, P->q, g);
   if (P->table_bits == 0) return 0;
@@ -155,6 +168,8 @@ int mo_machine_shape(const mo_params* P, size_t m, mo_shape* S) {
   size_t mp = S->L / S->k;
   if (mp > w / S->k) mp = w / S->k;
   S->m_prime = (unsigned)mp;
+  if (multi_probe(P) && (S->m_prime != 1 || S->k != 1 || P->table_bits < 6 || P->probes > 4))
+    return MO_ERR_CONFIG;
   S->match_mask = 0;
   S->boundary_keep = ~0ull;
   for (unsigned j = 0; j < S->k; ++j) {
@@ -179,6 +194,11 @@ int mo_build_masks(const mo_params* P, const uint8_t* pat_bytes, const size_t* l
         const uint8_t* g = og ? p + j : p + s + j * q;
         size_t align = j % S->k, pos = j / S->k;
         if (pos >= S->m_prime) continue;
+        if (multi_probe(P)) {
+          uint32_t h = mo_gram_hash(g, q);
+          for (unsigned i = 0; i < P->probes; ++i) masks[probe_entry(P, h, i)] &= ~1ull;
+          continue;
+        }
         masks[gram_index(P, g)] &= ~(1ull << (align * S->m_prime + pos));
       }
     }
@@ -313,7 +333,16 @@ int mo_search(const uint8_t* text, size_t n, const uint8_t* pat_bytes, const siz
     uint64_t u = og ? t : (t + 1) * k - 1;
     const uint8_t* g = text + (og ? u : u * q);
     ++reads;
-    d = ((d << 1) & S.boundary_keep) | masks[gram_index(P, g)];
+    uint64_t mv;
+    if (multi_probe(P)) {
+      uint32_t h = mo_gram_hash(g, q);
+      mv = 0;
+      for (unsigned i = 0; i < P->probes; ++i) mv |= masks[probe_entry(P, h, i)] & 1ull;
+      mv |= ~1ull;
+    } else {
+      mv = masks[gram_index(P, g)];
+    }
+    d = ((d << 1) & S.boundary_keep) | mv;
     if ((d & S.match_mask) == S.match_mask) continue;
     uint64_t hits = ~d & S.match_mask;
     while (hits) {

@@ -28,6 +28,7 @@ typedef struct mo_params {
   unsigned table_bits;  /* hashed: 2^table_bits mask entries */
   uint32_t sigma_prime; /* exact: map size */
   int window_rule;      /* MO_WINDOW_* */
+  unsigned probes;      /* hashed, m' = k = 1: entries probed per gram (0/1 = one) */
   uint8_t map[256];     /* exact: byte -> code */
 } mo_params;
 

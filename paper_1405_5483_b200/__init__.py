@@ -80,7 +80,7 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("table_in_smem", C.c_int), ("key_len", C.c_uint32), ("prefilter_bits", C.c_uint32),
         ("bucket_bits", C.c_uint32), ("tile_bytes", C.c_uint32), ("halo", C.c_uint32),
         ("warps", C.c_uint32), ("stages", C.c_uint32), ("smem_bytes", C.c_size_t),
-        ("predicted_candidates_per_byte", C.c_double),
+        ("predicted_candidates_per_byte", C.c_double), ("probes", C.c_uint32),
     ]
 
 

@@ -133,6 +133,7 @@ struct mag_engine {
   // device tables
   void* d_table = nullptr;
   uint32_t* d_prefilter = nullptr;
+  uint32_t* d_l2map = nullptr;
   uint32_t* d_bucket_start = nullptr;
   uint32_t* d_entries = nullptr;
   uint8_t* d_pat_bytes = nullptr;
@@ -151,6 +152,7 @@ struct mag_engine {
       cudaSetDevice(device);
       cudaFree(d_table);
       cudaFree(d_prefilter);
+      cudaFree(d_l2map);
       cudaFree(d_bucket_start);
       cudaFree(d_entries);
       cudaFree(d_pat_bytes);
@@ -296,6 +298,7 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.table = e->d_table;
     a.prefilter = e->d_prefilter;
     a.bucket_start = e->d_bucket_start;
+    a.l2map = e->d_l2map;
     a.bucket_entries = reinterpret_cast<const uint2*>(e->d_entries);
     a.pat_bytes = e->d_pat_bytes;
     a.pat_off = e->d_pat_off;
@@ -409,6 +412,7 @@ mag_status upload_engine(mag_engine* e) {
   MAG_CUDA(cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, e->device));
   MAG_CUDA(upload(e->table, reinterpret_cast<uint8_t**>(&e->d_table)));
   MAG_CUDA(upload(e->ptab.prefilter, &e->d_prefilter));
+  MAG_CUDA(upload(e->ptab.l2map, &e->d_l2map));
   MAG_CUDA(upload(e->ptab.bucket_start, &e->d_bucket_start));
   MAG_CUDA(upload(e->ptab.entries, &e->d_entries));
   MAG_CUDA(upload(e->pd.bytes, &e->d_pat_bytes));
@@ -586,6 +590,7 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->stages = P.ring;
   out->smem_bytes = plan_smem(P);
   out->predicted_candidates_per_byte = P.pred_cand_per_byte;
+  out->probes = P.sp.probes;
   return MAG_OK;
 }
 

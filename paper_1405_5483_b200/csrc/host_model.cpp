@@ -240,9 +240,10 @@ double prefilter_fp(double keys, unsigned pf_bits) {
 // DESIGN.md): per sample gram+lookup, per extra m' a shuffle, per candidate
 // a queue slot, per verified start a rolled key + prefilter, per prefilter
 // pass an L2 bucket probe.
-constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 10, kCostStart = 45,
-                 kCostWindow = 45, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40,
-                 kCostChunk = 4800;  // per staged chunk (loader + bookkeeping), thread-instr
+constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 45,
+                 kCostWindow = 60, kCostScreen = 25, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40,
+                 kCostChunk = 4800,  // per staged chunk (loader + bookkeeping), thread-instr
+                 kCostProbeBit = 3;  // per extra probe bit of a multi-probe gram
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -325,6 +326,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     return kBadConfig;
   }
   sp.overlapping = rq.variant == 2;
+  sp.probes = 1;
   sp.smag = rq.variant == 1;
   sp.m = static_cast<uint32_t>(std::min<size_t>(pd.m, 0xffffffffu));
   sp.maxlen = static_cast<uint32_t>(std::min<size_t>(pd.maxlen, 0xffffffffu));
@@ -411,7 +413,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     const double keys = static_cast<double>(pd.r);
     struct Cand {
       double cost = std::numeric_limits<double>::infinity();
-      unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 0;
+      unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 0, H = 1;
       uint32_t chunk = kChunkTarget;
       bool va = true;
       double cpb = 1;
@@ -457,10 +459,18 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                                          static_cast<unsigned>(wkey ? std::min<size_t>(16, m - q + 1)
                                                                     : std::min<size_t>(16, m)));
             for (unsigned tbits = 12; tbits <= 24; ++tbits) {
-              if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
+             if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
+             const unsigned hmax = (!sp.overlapping && mp == 1 && k == 1 && tbits >= 8) ? 4 : 1;
+             for (unsigned H = 1; H <= hmax; ++H) {
               const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
               const double adm = sp.overlapping ? keys : keys * q;
-              const double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
+              double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
+              if (H > 1) {  // probes inside a 32-entry block (est. as a plain Bloom filter)
+                const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
+                const double exact = universe > 1e15 ? 0.0 : distinct / universe;
+                const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / std::ldexp(1.0, static_cast<int>(tbits)));
+                p = exact + (1.0 - exact) * std::pow(fill, static_cast<double>(H));
+              }
               const double pm = std::pow(p, static_cast<double>(mp));
               // candidates per byte, and verified starts per byte
               const double cpb = sp.overlapping ? pm : pm / q;
@@ -475,9 +485,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                 }
                 if (!chunk) continue;
                 const double fp = pf ? prefilter_fp(nkeys, pf) : 1.0;
-                double cost = sample_cost + kCostChunk / chunk;
-                if (wkey)  // window keys: one probe per candidate
-                  cost += cpb * (kCostCand + kCostWindow + fp * kCostProbe + hits * kCostCompare);
+                double cost = sample_cost + (H - 1) * kCostProbeBit / (k * q) + kCostChunk / chunk;
+                if (wkey)  // window keys: one batched key + L2 screen per candidate
+                  cost += cpb * (kCostCand + kCostWindow + fp * (kCostScreen + 0.01 * kCostProbe) +
+                                 hits * kCostCompare);
                 else       // start keys: one probe per verified start
                   cost += cpb * kCostCand + pm * (kCostStart + fp * kCostProbe + hits * kCostCompare);
                 if (cost < best.cost * 0.999) {
@@ -486,12 +497,14 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                   best.k = k;
                   best.mp = mp;
                   best.tb = tbits;
+                  best.H = H;
                   best.pf = pf;
                   best.chunk = chunk;
                   best.va = false;
                   best.cpb = cpb;
                 }
               }
+             }
             }
           }
         }
@@ -510,6 +523,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.m_prime = best.mp;
       sp.table_bits = best.tb;
       sp.entries = 1ull << best.tb;
+      sp.probes = best.H;
     }
     sp.pf_bits = best.pf;
     P->chunk_target = best.chunk;
@@ -560,6 +574,12 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
+  sp.l2_bits = 0;
+  if (sp.window_key) {  // ~128 bits per key: ~0.8% of screened keys walk a bucket
+    unsigned lb = 16;
+    while (lb < 30 && (size_t(1) << lb) < 128 * pd.r * sp.q) ++lb;
+    sp.l2_bits = lb;
+  }
   {
     const size_t keys = sp.window_key ? pd.r * sp.q : pd.r;
     unsigned bb = 4;
@@ -590,6 +610,11 @@ static inline uint32_t gram_index_host(const Plan& P, const uint8_t* g) {
     return code;
   }
   return gram_slot(hash_gram_bytes(g, sp.q), sp.table_bits);
+}
+
+// Entries of a gram under multi-probe hashing (probes >= 2).
+static inline uint32_t probe_entry(const ScanPlan& sp, uint32_t h, unsigned i) {
+  return (probe_block(h, sp.table_bits) << 5) | probe_bit(h, i);
 }
 
 static inline void clear_bit(const Plan& P, std::vector<uint8_t>* t, uint64_t idx, unsigned b) {
@@ -637,6 +662,11 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
         const size_t align = c % sp.k, pos = c / sp.k;
         if (pos >= sp.m_prime) continue;
         const uint8_t* g = sp.overlapping ? p + c : p + s + c * q;
+        if (sp.probes > 1) {
+          const uint32_t hh = hash_gram_bytes(g, q);
+          for (unsigned i = 0; i < sp.probes; ++i) clear_bit(P, table, probe_entry(sp, hh, i), 0);
+          continue;
+        }
         clear_bit(P, table, gram_index_host(P, g),
                   static_cast<unsigned>(align * sp.m_prime + pos));
       }
@@ -674,6 +704,14 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
       const uint32_t i2 = ((e.key ^ (e.key >> 15)) * 0x2C1B3C6Du) >> (32 - sp.pf_bits);
       pt->prefilter[i1 >> 5] |= 1u << (i1 & 31);
       pt->prefilter[i2 >> 5] |= 1u << (i2 & 31);
+    }
+  }
+  // L2 screen bitmap (window keys): top key bits
+  pt->l2map.assign(sp.l2_bits ? std::max<size_t>(4, (size_t(1) << sp.l2_bits) / 32) : 4, 0);
+  if (sp.l2_bits) {
+    for (const Ent& e : ents) {
+      const uint32_t b = e.key >> (32 - sp.l2_bits);
+      pt->l2map[b >> 5] |= 1u << (b & 31);
     }
   }
   // buckets by low key bits, stable within a bucket

@@ -106,6 +106,7 @@ uint64_t mask_entry(const Plan& plan, const std::vector<uint8_t>& table, uint64_
 // Verification tables: prefilter bitmap, buckets, entries {key, pid}.
 struct PatternTable {
   std::vector<uint32_t> prefilter;
+  std::vector<uint32_t> l2map;
   std::vector<uint32_t> bucket_start;
   std::vector<uint32_t> entries;  // interleaved key, pid
 };

@@ -56,6 +56,14 @@ MAG_HD uint32_t gram_slot(uint32_t h, unsigned table_bits) {
   return table_bits ? (h >> (32 - table_bits)) : 0u;
 }
 
+// Multi-probe hashed grams (1-bit entries, probes >= 2): a gram owns
+// `probes` entries inside one 32-entry block of the table — block
+// h >> (37 - table_bits), entry bits taken from a second mix of h — and is
+// admitted only where all of them are admitted.  An intersection of hashed
+// q-gram alphabets: still never rejects a gram a pattern contributed.
+MAG_HD uint32_t probe_block(uint32_t h, unsigned table_bits) { return h >> (37 - table_bits); }
+MAG_HD uint32_t probe_bit(uint32_t h, unsigned i) { return ((h * 0x9E3779B1u) >> (27 - 5 * i)) & 31u; }
+
 // Verification key: the first v = min(m, 16) bytes of a start, read as four
 // little-endian words (bytes past v zeroed), mixed.  Top bits index the
 // shared-memory prefilter, low bits the bucket table.
@@ -95,6 +103,7 @@ struct ScanPlan {
   uint32_t q, k, m_prime;
   uint32_t sigma_prime;
   uint32_t table_bits;    // hashed: log2(entries)
+  uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..4)
   uint32_t entry_log2;    // log2(bits per mask entry), 0..6
   uint64_t entries;       // number of mask entries
   uint64_t table_bytes;   // packed table size (multiple of 16)
@@ -108,6 +117,9 @@ struct ScanPlan {
   // each hit naming the start q*ss - s directly.
   int window_key;
   uint32_t wkey_len;
+  // Window keys are screened by an L2-resident bitmap of 2^l2_bits bits
+  // (bit = key >> (32 - l2_bits)) before any bucket walk; 0 = no bitmap.
+  uint32_t l2_bits;
   uint32_t pf_bits;       // prefilter bitmap has 2^pf_bits bits (smem)
   uint32_t bucket_bits;   // 2^bucket_bits buckets (global)
   uint32_t r;
@@ -117,7 +129,8 @@ struct ScanPlan {
 // ---- shared-memory layout of the scan kernel (host computes the size,
 // device carves it; one definition for both).
 constexpr int kMaxWarps = 16;   // warps per CTA (launch bound: 512 threads)
-constexpr int kQueueCap = 64;   // candidate windows queued per warp
+constexpr int kQueueCap = 64;   // candidate windows queued per warp (per chunk)
+constexpr int kProbeCap = 128;  // window keys awaiting the L2 screen (per slice)
 
 // Per ring slot: what the staged bytes are.
 struct SlotInfo {
@@ -133,7 +146,7 @@ struct SlotInfo {
 MAG_HD size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct SmemLayout {
-  size_t table, pf, map, slots, info, queue, bars, total;
+  size_t table, pf, map, slots, info, queue, probe, bars, total;
 };
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,
@@ -152,6 +165,8 @@ MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t r
   o += align16(size_t(nwarps) * ring * sizeof(SlotInfo));
   L.queue = o;
   o += align16(size_t(nwarps) * kQueueCap * 4);
+  L.probe = o;
+  o += align16(size_t(nwarps) * kProbeCap * 8);
   L.bars = o;
   o += size_t(nwarps) * ring * 8;
   L.total = o;

@@ -110,6 +110,7 @@ struct Smem {
   uint8_t* slots;     // [warp][ring][slot_bytes]
   SlotInfo* info;     // [warp][ring]
   uint32_t* queue;    // [warp][kQueueCap]
+  uint2* probe;       // [warp][kProbeCap]
   uint64_t* bars;     // [warp][ring]
 };
 
@@ -135,6 +136,10 @@ struct Scanner {
   // slice output
   uint64_t* out;                // staging of the current slice
   uint32_t fill;                // matches written for the current slice
+  // window keys awaiting the L2 screen: {key, start position - pbase}
+  uint2* pq;
+  uint32_t pqn;
+  unsigned long long pbase;
   unsigned long long cands;
   // loader state (warp-uniform)
   unsigned long long ld_slice, ld_t, ld_tend;
@@ -149,7 +154,7 @@ struct Scanner {
   uint32_t inv_mp;              // bit / m' == (bit * inv_mp) >> 16
 
   __device__ Scanner(const ScanArgs& a, const Smem& s, int l, int w)
-      : A(a), S(s), lane(l), warp(w), fill(0), cands(0) {
+      : A(a), S(s), lane(l), warp(w), fill(0), pqn(0), pbase(0), cands(0) {
     const ScanPlan& P = A.plan;
     qk = P.overlapping || P.verify_all ? 1u : P.q * P.k;
     W = P.overlapping ? 1u : P.q;
@@ -165,6 +170,7 @@ struct Scanner {
     myinfo = S.info + static_cast<size_t>(w) * A.ring;
     mybars = S.bars + static_cast<size_t>(w) * A.ring;
     queue = S.queue + static_cast<size_t>(w) * kQueueCap;
+    pq = S.probe + static_cast<size_t>(w) * kProbeCap;
     ld_slice = 0;
     ld_t = ld_tend = 0;
     ld_done = false;
@@ -289,9 +295,24 @@ struct Scanner {
 #pragma unroll
         for (int i = 0; i < QW; ++i) x[i] = __funnelshift_r(w[i], w[i + 1], sh);
       }
-      const uint32_t rem = P.q - 4u * (QW - 1);  // 1..4 bytes in the last word
-      x[QW - 1] &= rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
-      return table_entry(hash_gram_words(x[0], x[1], x[2], x[3]) >> (32 - P.table_bits));
+      if constexpr (!A4) {  // q % 4 == 0 fills the last word
+        const uint32_t rem = P.q - 4u * (QW - 1);  // 1..4 bytes in the last word
+        x[QW - 1] &= rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
+      }
+      const uint32_t h = hash_gram_words(x[0], x[1], x[2], x[3]);
+      if constexpr (CMP == 1 && CK == 1 && sizeof(E) == 4 && TSMEM) {
+        if (P.probes > 1) {
+          // multi-probe: one block word, all probed entries must admit
+          const uint32_t blk = static_cast<const uint32_t*>(S.table)[probe_block(h, P.table_bits)];
+          const uint32_t g = h * 0x9E3779B1u;
+          uint32_t m = blk >> (g >> 27);
+          m |= blk >> ((g >> 22) & 31u);
+          if (P.probes > 2) m |= blk >> ((g >> 17) & 31u);
+          if (P.probes > 3) m |= blk >> ((g >> 12) & 31u);
+          return static_cast<E>(m & 1u);
+        }
+      }
+      return table_entry(h >> (32 - P.table_bits));
     } else {
       const uint32_t q = P.q, sp = P.sigma_prime;
       uint32_t code = S.map[sb[rel + q - 1]];
@@ -387,10 +408,22 @@ struct Scanner {
     fill += total;
   }
 
-  // Window keys: the key at slot offset r0 (= gram boundary q*ss) against
-  // the (pattern, shift) index; entry shift s names start r0 - s.  Entries
-  // come in (shift descending, pattern ascending) order = text order.
-  __device__ uint32_t probe_window(uint32_t r0, uint32_t key, uint64_t* dst, uint32_t idx) const {
+  // Window keys: a candidate window's key (read at its gram boundary
+  // a0 = q*ss while the chunk is staged) against the (pattern, shift)
+  // index; entry shift s names start a0 - s.  Entries come in (shift
+  // descending, pattern ascending) order = text order.  Key hits are rare
+  // (true matches and 32-bit key collisions) and compare against the text in
+  // global memory, so queued keys outlive the staged chunk.
+  __device__ bool equal_global(unsigned long long a, uint32_t pid, uint32_t len) const {
+    const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
+    const uint8_t* t = A.text + a;
+    for (uint32_t i = 0; i < len; ++i)
+      if (__ldg(t + i) != __ldg(p + i)) return false;
+    return true;
+  }
+
+  __device__ uint32_t probe_window(unsigned long long a0, uint32_t key, uint64_t* dst,
+                                   uint32_t idx) const {
     const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
     const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
     uint32_t c = 0;
@@ -398,40 +431,77 @@ struct Scanner {
       const uint2 ent = __ldg(A.bucket_entries + e);
       if (ent.x != key) continue;
       const uint32_t s = ent.y >> kPidBits, pid = ent.y & ((1u << kPidBits) - 1u);
-      if (s > r0 + src) continue;  // start before the text
-      const uint32_t r = r0 - s;
-      const unsigned long long a = src + r;
+      if (s > a0) continue;  // start before the text
+      const unsigned long long a = a0 - s;
       const uint32_t len = __ldg(A.pat_len + pid);
-      if (a + len > A.n || !equal_at(r, pid, len)) continue;
+      if (a + len > A.n || !equal_global(a, pid, len)) continue;
       if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, pid);
       ++c;
     }
     return c;
   }
 
-  // One candidate window per lane, in queue (= text) order.
-  __device__ void drain_windows(uint32_t qlen, long long ss_ref) {
+  // Screen + verify the probe queue: 4 consecutive keys per lane (lane-major
+  // = text order); the four L2 bitmap loads are independent, so one round
+  // trip covers 128 windows.  Survivors walk their bucket.
+  __device__ void flush_pq() {
     __syncwarp();
-    const uint32_t q = A.plan.q, v = A.plan.wkey_len;
-    // slot offset of the gram boundary q*ss of queue entry 0
-    const long long base0 = ss_ref * static_cast<long long>(q) - static_cast<long long>(src);
-    const long long lim = static_cast<long long>(A.n) - static_cast<long long>(src) - v;  // key must fit
-    for (uint32_t i0 = 0; i0 < qlen; i0 += 32) {
-      const uint32_t i = i0 + lane;
-      uint32_t key = 0, c = 0, r0 = 0;
-      if (i < qlen) {
-        const long long rr = base0 + static_cast<long long>(queue[i]) * q;
-        if (rr >= 0 && rr <= lim) {
-          r0 = static_cast<uint32_t>(rr);
-          key = key_at(r0, v);
-          if (prefilter_pass(key)) c = probe_window(r0, key, nullptr, 0);
-        }
+    const uint32_t lb = A.plan.l2_bits;
+    for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
+      const uint32_t i0 = b0 + 4 * lane;
+      uint2 e[4];
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
+        w[j] = 1u;
+        if (lb && e[j].y != 0xffffffffu) w[j] = __ldg(A.l2map + ((e[j].x >> (32 - lb)) >> 5));
+      }
+      uint32_t cnt[4], c = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cnt[j] = 0;
+        const bool live = e[j].y != 0xffffffffu && (!lb || ((w[j] >> ((e[j].x >> (32 - lb)) & 31u)) & 1u));
+        if (live) cnt[j] = probe_window(pbase + e[j].y, e[j].x, nullptr, 0);
+        c += cnt[j];
       }
       if (!__any_sync(kFull, c != 0)) continue;
       const uint32_t excl = warp_excl_scan(c, lane);
       const uint32_t total = __shfl_sync(kFull, excl + c, 31);
-      if (c) probe_window(r0, key, out, fill + excl);
+      uint32_t at = fill + excl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (cnt[j]) at += probe_window(pbase + e[j].y, e[j].x, out, at);
       fill += total;
+    }
+    pqn = 0;
+    __syncwarp();
+  }
+
+  // Queued candidate windows -> keys (read from the staged chunk now) in the
+  // probe queue.  Windows whose key would run past the text cannot match.
+  __device__ void drain_windows(uint32_t qlen, long long ss_ref) {
+    __syncwarp();
+    const uint32_t q = A.plan.q, v = A.plan.wkey_len;
+    for (uint32_t i0 = 0; i0 < qlen; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      bool ok = false;
+      uint32_t key = 0;
+      unsigned long long a0 = 0;
+      if (i < qlen) {
+        a0 = static_cast<unsigned long long>(ss_ref + static_cast<long long>(queue[i])) * q;
+        ok = a0 + v <= A.n;
+        if (ok) {
+          key = key_at(static_cast<uint32_t>(a0 - src), v);
+          ok = prefilter_pass(key);
+        }
+      }
+      const unsigned bal = __ballot_sync(kFull, ok);
+      if (!bal) continue;
+      if (pqn + __popc(bal) > kProbeCap) flush_pq();
+      if (ok) pq[pqn + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
+      __syncwarp();
+      pqn += __popc(bal);
     }
     __syncwarp();
   }
@@ -600,10 +670,17 @@ struct Scanner {
       sw = reinterpret_cast<const uint32_t*>(sb);
       src = in.src;
       valid = in.valid;
-      if (in.flags & 1u) fill = 0;
+      if (in.flags & 1u) {
+        fill = 0;
+        pqn = 0;
+        pbase = in.src;
+      }
       out = A.staging + static_cast<size_t>(in.slice) * A.slice_cap;
       process_chunk(in);
-      if ((in.flags & 2u) && lane == 0) A.slice_count[in.slice] = fill;
+      if (in.flags & 2u) {
+        if (pqn) flush_pq();
+        if (lane == 0) A.slice_count[in.slice] = fill;
+      }
       __syncwarp();
       ++cons;
       issue();
@@ -626,6 +703,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
   S.slots = smem + L.slots;
   S.info = reinterpret_cast<SlotInfo*>(smem + L.info);
   S.queue = reinterpret_cast<uint32_t*>(smem + L.queue);
+  S.probe = reinterpret_cast<uint2*>(smem + L.probe);
   S.bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   {
     const int tid = threadIdx.x, nt = blockDim.x;

@@ -23,6 +23,7 @@ struct ScanArgs {
   const void* table;            // packed mask table (global copy)
   const uint32_t* prefilter;    // 2^pf_bits bits
   const uint32_t* bucket_start; // 2^bucket_bits + 1
+  const uint32_t* l2map;        // 2^l2_bits-bit key bitmap (window keys)
   const uint2* bucket_entries;  // {key hash, pattern id}, r entries
   const uint8_t* pat_bytes;     // 16-byte aligned, zero padded per pattern
   const uint64_t* pat_off;

@@ -16,12 +16,19 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--iters", type=int, default=4)
 ap.add_argument("--opts", default="", help="engine kwargs, e.g. tile_bytes=16384,warps=8")
+ap.add_argument("--r", type=int, default=0, help="replace the pattern set by r iid patterns (length m)")
 a = ap.parse_args()
 kw = {}
 for kv in filter(None, a.opts.split(",")):
     k, v = kv.split("=")
     kw[k] = int(v) if v.lstrip("-").isdigit() else v
 w = workloads.generate(a.config, a.scale)
+if a.r:
+    import numpy as np
+    rng = np.random.default_rng(7)
+    m = w.meta["m"]
+    alpha = np.unique(w.text[: 1 << 20])
+    w.patterns = [alpha[rng.integers(0, alpha.size, m)].tobytes() for _ in range(a.r)]
 e = mag.Engine(w.patterns, **kw)
 d = torch.from_numpy(w.text).cuda()
 p = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
