@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -292,6 +293,7 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   if (g.num_slices) {
     ScanArgs a{};
     a.plan = P.sp;
+    if (const char* d = std::getenv("MAG_B200_DIAG")) a.plan.diag = std::atoi(d);  // profiling only
     a.text = d_text;
     a.n = n;
     a.codes = d_codes;

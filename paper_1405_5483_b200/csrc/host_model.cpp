@@ -272,6 +272,12 @@ void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
   const uint32_t m16 = 16 / gcd32(16, bps);
   uint32_t c = std::max<uint32_t>(32, target / bps / m16 * m16);
   c = (c + m16 - 1) / m16 * m16;
+  // k = 1 strided chunks record hits in a <= 1024-bit bitmap; m' = 1 chunks
+  // tile into whole 64-sample steps
+  if (!sp.overlapping && !sp.verify_all && sp.k == 1) {
+    c = std::min<uint32_t>(c, 1024);
+    if (sp.m_prime == 1 && c >= 64 && 64 % m16 == 0) c = c / 64 * 64;
+  }
   P->chunk_samples = c;
   const uint64_t chunk_bytes = static_cast<uint64_t>(c) * bps;
   P->slice_samples = static_cast<uint64_t>(c) *

@@ -120,6 +120,8 @@ struct ScanPlan {
   // Window keys are screened by an L2-resident bitmap of 2^l2_bits bits
   // (bit = key >> (32 - l2_bits)) before any bucket walk; 0 = no bitmap.
   uint32_t l2_bits;
+  // diagnostics only (MAG_B200_DIAG env): 1 = skip candidate verification
+  int diag;
   uint32_t pf_bits;       // prefilter bitmap has 2^pf_bits bits (smem)
   uint32_t bucket_bits;   // 2^bucket_bits buckets (global)
   uint32_t r;
@@ -131,6 +133,7 @@ struct ScanPlan {
 constexpr int kMaxWarps = 16;   // warps per CTA (launch bound: 512 threads)
 constexpr int kQueueCap = 64;   // candidate windows queued per warp (per chunk)
 constexpr int kProbeCap = 128;  // window keys awaiting the L2 screen (per slice)
+constexpr int kHitWords = 32;   // per-chunk hit bitmap (chunks of <= 1024 samples, k = 1)
 
 // Per ring slot: what the staged bytes are.
 struct SlotInfo {
@@ -146,7 +149,7 @@ struct SlotInfo {
 MAG_HD size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct SmemLayout {
-  size_t table, pf, map, slots, info, queue, probe, bars, total;
+  size_t table, pf, map, slots, info, queue, probe, hits, bars, total;
 };
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,
@@ -167,6 +170,8 @@ MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t r
   o += align16(size_t(nwarps) * kQueueCap * 4);
   L.probe = o;
   o += align16(size_t(nwarps) * kProbeCap * 8);
+  L.hits = o;
+  o += align16(size_t(nwarps) * kHitWords * 4);
   L.bars = o;
   o += size_t(nwarps) * ring * 8;
   L.total = o;

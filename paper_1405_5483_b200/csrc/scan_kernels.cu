@@ -111,6 +111,7 @@ struct Smem {
   SlotInfo* info;     // [warp][ring]
   uint32_t* queue;    // [warp][kQueueCap]
   uint2* probe;       // [warp][kProbeCap]
+  uint32_t* hits;     // [warp][kHitWords]
   uint64_t* bars;     // [warp][ring]
 };
 
@@ -139,6 +140,8 @@ struct Scanner {
   // window keys awaiting the L2 screen: {key, start position - pbase}
   uint2* pq;
   uint32_t pqn;
+  uint32_t* hbm;                // hit bitmap of the chunk (k = 1 strided)
+  uint32_t cands32;             // candidates since the last fold into `cands`
   unsigned long long pbase;
   unsigned long long cands;
   // loader state (warp-uniform)
@@ -171,6 +174,8 @@ struct Scanner {
     mybars = S.bars + static_cast<size_t>(w) * A.ring;
     queue = S.queue + static_cast<size_t>(w) * kQueueCap;
     pq = S.probe + static_cast<size_t>(w) * kProbeCap;
+    hbm = S.hits + static_cast<size_t>(w) * kHitWords;
+    cands32 = 0;
     ld_slice = 0;
     ld_t = ld_tend = 0;
     ld_done = false;
@@ -584,6 +589,100 @@ struct Scanner {
     }
   }
 
+  // k = 1 strided chunk: the filter only records hit ballots (one bit per
+  // sample, in a per-chunk bitmap); the bitmap is expanded into candidate
+  // windows once at the end of the chunk.
+  __device__ void bitmap_chunk(const SlotInfo& in, int mp) {
+    const ScanPlan& P = A.plan;
+    const int nsamp = static_cast<int>(in.nsamp);
+    const int ov = mp - 1;
+    const int g0 = static_cast<int>(((in.t0 + 1) * P.k - 1) * P.q - src);
+    const int gstep = static_cast<int>(P.q);
+    const long long ss_ref = static_cast<long long>(in.t0) - ov;  // ss = ss_ref + t_rel
+    const int tmin = in.t0 < static_cast<unsigned long long>(ov) ? -static_cast<int>(in.t0) : -ov;
+    const int thit = in.t0 < static_cast<unsigned long long>(ov) ? ov - static_cast<int>(in.t0) : 0;
+    const E mm = static_cast<E>(P.match_mask);
+    const E ones = static_cast<E>(~E(0));
+    const int nwords = (nsamp + 31) >> 5;
+    if (lane < nwords) hbm[lane] = 0u;
+    __syncwarp();
+    if (CMP == 1 && (nsamp & 63) == 0 && thit == 0) {
+      // interior m' = 1 chunk: every lane valid, hits are ~mask & 1
+      for (int base = 0; base < nsamp; base += 64) {
+        const int ta = base + lane, tb = ta + 32;
+        const E ma = gram_mask(static_cast<uint32_t>(g0 + ta * gstep), in.t0 + ta);
+        const E mb = gram_mask(static_cast<uint32_t>(g0 + tb * gstep), in.t0 + tb);
+        const unsigned ba = __ballot_sync(kFull, !(ma & mm));
+        const unsigned bb = __ballot_sync(kFull, !(mb & mm));
+        if (lane == 0) {
+          hbm[base >> 5] = ba;
+          hbm[(base >> 5) + 1] = bb;
+        }
+      }
+    } else {
+      const int lead = ov;
+      for (int base = -lead; base + lead < nsamp; base += 64 - lead) {
+        const int ta = base + lane, tb = ta + 32;
+        const bool va = ta >= tmin && ta < nsamp, vb = tb < nsamp;
+        const E ma = gram_mask(static_cast<uint32_t>(va ? g0 + ta * gstep : 0), in.t0 + (va ? ta : 0));
+        const E mb = gram_mask(static_cast<uint32_t>(vb ? g0 + tb * gstep : 0), in.t0 + (vb ? tb : 0));
+        const E Ma = va ? ma : ones, Mb = vb ? mb : ones;
+        E Da = Ma, Db = Mb;
+#pragma unroll
+        for (int i = 1; i <= (CMP ? CMP - 1 : 15); ++i) {
+          if (!CMP && i > ov) break;
+          const E ua = shfl_up_e(Ma, i);
+          const E ub = shfl_up_e(Mb, i);
+          const E wa = __shfl_sync(kFull, Ma, (lane - i) & 31);
+          Da |= static_cast<E>(ua << i);
+          Db |= static_cast<E>((lane >= i ? ub : wa) << i);
+        }
+        const unsigned ba = __ballot_sync(kFull, lane >= lead && ta >= thit && ta < nsamp && !(Da & mm));
+        const unsigned bb = __ballot_sync(kFull, tb >= thit && tb < nsamp && !(Db & mm));
+        if (lane == 0) {
+          // samples [base, base + 64) -> bits; base may be unaligned (m' > 1)
+          const int s0 = base + 32 * 0, s1 = base + 32;
+          if (ba) {
+            const int w = s0 >> 5, off = s0 & 31;  // s0 >= -lead: lanes < lead carry no bits
+            if (s0 >= 0) {
+              hbm[w] |= ba << off;
+              if (off && w + 1 < kHitWords) hbm[w + 1] |= ba >> (32 - off);
+            } else {
+              hbm[0] |= ba >> (-s0);
+            }
+          }
+          if (bb) {
+            const int w = s1 >> 5, off = s1 & 31;
+            hbm[w] |= bb << off;
+            if (off && w + 1 < kHitWords) hbm[w + 1] |= bb >> (32 - off);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // expand: lane l owns bitmap word l; candidate ranks in text order
+    const uint32_t word = lane < nwords ? hbm[lane] : 0u;
+    const uint32_t cnt = __popc(word);
+    cands32 += cnt;
+    const uint32_t excl = warp_excl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
+    if (P.diag & 1) return;
+    for (uint32_t r0 = 0; r0 < total; r0 += kQueueCap) {
+      if (cnt && excl < r0 + kQueueCap && excl + cnt > r0) {
+        uint32_t wv = word, rank = excl;
+        while (wv) {
+          const int b = __ffs(wv) - 1;
+          wv &= wv - 1;
+          if (rank >= r0 && rank < r0 + kQueueCap) queue[rank - r0] = static_cast<uint32_t>(32 * lane + b);
+          ++rank;
+        }
+      }
+      __syncwarp();
+      const uint32_t qn = total - r0 < static_cast<uint32_t>(kQueueCap) ? total - r0 : kQueueCap;
+      drain(qn, ss_ref);
+    }
+  }
+
   __device__ void process_chunk(const SlotInfo& in) {
     const ScanPlan& P = A.plan;
     const int nsamp = static_cast<int>(in.nsamp);
@@ -600,6 +699,10 @@ struct Scanner {
     const int ov = mp - 1;
     const int k = CK ? CK : this->k;
     const uint32_t inv_mp = CMP ? (65536u + CMP - 1) / CMP : this->inv_mp;
+    if (k == 1 && !P.overlapping && mp <= 16) {
+      bitmap_chunk(in, mp);
+      return;
+    }
     // slot offset of the gram of relative sample 0, and per-sample stride
     const int g0 = static_cast<int>(
         (P.overlapping ? in.t0 : ((in.t0 + 1) * P.k - 1) * P.q) - src);
@@ -685,7 +788,7 @@ struct Scanner {
       ++cons;
       issue();
     }
-    unsigned long long c = cands;
+    unsigned long long c = cands + cands32;
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
     if (lane == 0 && c) atomicAdd(A.counters + 1, c);
@@ -704,6 +807,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
   S.info = reinterpret_cast<SlotInfo*>(smem + L.info);
   S.queue = reinterpret_cast<uint32_t*>(smem + L.queue);
   S.probe = reinterpret_cast<uint2*>(smem + L.probe);
+  S.hits = reinterpret_cast<uint32_t*>(smem + L.hits);
   S.bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   {
     const int tid = threadIdx.x, nt = blockDim.x;
