@@ -33,6 +33,7 @@ typedef struct mag_options_ex {
   int warps;       /* consumer warps per CTA, 0 = auto (<= 16) */
   int stages;      /* TMA ring depth, 0 = auto */
   int device;      /* CUDA device ordinal, -1 = current */
+  int probes;      /* hashed: table entries probed per gram, 0 = auto */
 } mag_options_ex;
 
 MAG_API void mag_options_ex_init(mag_options_ex* opts);
@@ -58,6 +59,8 @@ typedef struct mag_plan_info {
   size_t smem_bytes;
   double predicted_candidates_per_byte;
   uint32_t probes;      /* hashed, m' = k = 1: table entries probed per gram */
+  uint32_t blocks;      /* probes >= 2: 64-entry table blocks */
+  int direct;           /* q = 16 stream kernel */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

@@ -110,12 +110,13 @@ uint32_t mo_gram_hash(const uint8_t* p, unsigned q) {
 }
 
 /* Multi-probe hashed grams (GPU extension; paper_1405_5483_b200/csrc/
- * mag_common.h probe_block/probe_bit): `probes` entries inside one 32-entry
+ * mag_common.h bloom_block/bloom_bit): `probes` entries of one 64-entry
  * block, admitted only where all of them are admitted. */
 static inline uint32_t probe_entry(const mo_params* P, uint32_t h, unsigned i) {
-  uint32_t blk = h >> (37 - P->table_bits);
-  uint32_t bit = ((h * 0x9E3779B1u) >> (27 - 5 * i)) & 31u;
-  return (blk << 5) | bit;
+  uint32_t blk = (uint32_t)(((uint64_t)h * P->blocks) >> 32);
+  uint64_t g = (uint64_t)h * 0x9E3779B97F4A7C15ull;
+  uint32_t bit = (uint32_t)(g >> (58 - 6 * i)) & 63u;
+  return blk * 64u + bit;
 }
 
 static inline int multi_probe(const mo_params* P) {
@@ -151,7 +152,7 @@ int mo_machine_shape(const mo_params* P, size_t m, mo_shape* S) {
     S->entries = space;
   } else {
     if (q > 16 || P->table_bits > 26) return MO_ERR_CONFIG;
-    S->entries = (uint64_t)1 << P->table_bits;
+    S->entries = P->probes > 1 ? (uint64_t)P->blocks * 64 : (uint64_t)1 << P->table_bits;
   }
   if (og) {
     if (m < q) return MO_ERR_CONFIG;
@@ -168,7 +169,7 @@ int mo_machine_shape(const mo_params* P, size_t m, mo_shape* S) {
   size_t mp = S->L / S->k;
   if (mp > w / S->k) mp = w / S->k;
   S->m_prime = (unsigned)mp;
-  if (multi_probe(P) && (S->m_prime != 1 || S->k != 1 || P->table_bits < 6 || P->probes > 4))
+  if (multi_probe(P) && (S->m_prime != 1 || S->k != 1 || P->blocks < 1 || P->probes > 8))
     return MO_ERR_CONFIG;
   S->match_mask = 0;
   S->boundary_keep = ~0ull;

@@ -29,6 +29,7 @@ typedef struct mo_params {
   uint32_t sigma_prime; /* exact: map size */
   int window_rule;      /* MO_WINDOW_* */
   unsigned probes;      /* hashed, m' = k = 1: entries probed per gram (0/1 = one) */
+  unsigned blocks;      /* probes >= 2: 64-entry blocks (table = 64 * blocks entries) */
   uint8_t map[256];     /* exact: byte -> code */
 } mo_params;
 

@@ -183,7 +183,7 @@ class _MoParams(C.Structure):
     _fields_ = [
         ("variant", C.c_int), ("gram_mode", C.c_int), ("q", C.c_uint), ("k", C.c_uint),
         ("word_bits", C.c_uint), ("table_bits", C.c_uint), ("sigma_prime", C.c_uint32),
-        ("window_rule", C.c_int), ("probes", C.c_uint), ("map", C.c_uint8 * 256),
+        ("window_rule", C.c_int), ("probes", C.c_uint), ("blocks", C.c_uint), ("map", C.c_uint8 * 256),
     ]
 
 
@@ -238,9 +238,10 @@ class Port:
 
     @staticmethod
     def params(variant=0, gram_mode=0, q=1, k=1, word_bits=64, table_bits=0, sigma_prime=256,
-               table: Optional[bytes] = None, window_rule=0, probes=1) -> _MoParams:
+               table: Optional[bytes] = None, window_rule=0, probes=1, blocks=0) -> _MoParams:
         p = _MoParams()
         p.probes = probes
+        p.blocks = blocks
         p.variant, p.gram_mode, p.q, p.k = variant, gram_mode, q, k
         p.word_bits, p.table_bits, p.sigma_prime, p.window_rule = word_bits, table_bits, sigma_prime, window_rule
         t = table if table is not None else bytes(range(256))

@@ -508,6 +508,7 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     rq.tile_bytes = opts.tile_bytes;
     rq.warps = opts.warps;
     rq.stages = opts.stages;
+    rq.probes = opts.probes;
     if (opts.base.q < 0 || opts.base.k < 0 || opts.base.sigma_prime < 0)
       return fail(MAG_ERR_BAD_CONFIG, "q, k and sigma' must be >= 0 (0 = auto)");
     if (opts.base.mapping < -1 || opts.base.mapping > 3)
@@ -593,6 +594,8 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->smem_bytes = plan_smem(P);
   out->predicted_candidates_per_byte = P.pred_cand_per_byte;
   out->probes = P.sp.probes;
+  out->blocks = P.sp.blocks;
+  out->direct = P.sp.direct;
   return MAG_OK;
 }
 

@@ -243,7 +243,8 @@ double prefilter_fp(double keys, unsigned pf_bits) {
 constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 45,
                  kCostWindow = 60, kCostScreen = 25, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40,
                  kCostChunk = 4800,  // per staged chunk (loader + bookkeeping), thread-instr
-                 kCostProbeBit = 3;  // per extra probe bit of a multi-probe gram
+                 kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
+                 kCostPf = 15;       // shared-memory prefilter test
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -307,6 +308,7 @@ void set_entry_geometry(ScanPlan& sp) {
   uint64_t match = 0;
   for (unsigned j = 0; j < sp.k; ++j) match |= 1ull << (j * sp.m_prime + sp.m_prime - 1);
   sp.match_mask = match;
+  if (sp.probes > 1) sp.entries = static_cast<uint64_t>(sp.blocks) * 64;
   const uint64_t tbits = sp.entries << sp.entry_log2;
   sp.table_bytes = align16(std::max<uint64_t>(16, (tbits + 7) / 8));
 }
@@ -421,6 +423,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       double cost = std::numeric_limits<double>::infinity();
       unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 0, H = 1;
       uint32_t chunk = kChunkTarget;
+      int direct = 0;
+      uint32_t blocks = 0;
       bool va = true;
       double cpb = 1;
     } best;
@@ -468,6 +472,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
              if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
              const unsigned hmax = (!sp.overlapping && mp == 1 && k == 1 && tbits >= 8) ? 4 : 1;
              for (unsigned H = 1; H <= hmax; ++H) {
+              if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
               const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
               const double adm = sp.overlapping ? keys : keys * q;
               double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
@@ -493,8 +498,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                 const double fp = pf ? prefilter_fp(nkeys, pf) : 1.0;
                 double cost = sample_cost + (H - 1) * kCostProbeBit / (k * q) + kCostChunk / chunk;
                 if (wkey)  // window keys: one batched key + L2 screen per candidate
-                  cost += cpb * (kCostCand + kCostWindow + fp * (kCostScreen + 0.01 * kCostProbe) +
-                                 hits * kCostCompare);
+                  cost += cpb * (kCostCand + kCostWindow + (pf ? kCostPf : 0.0) +
+                                 fp * (kCostScreen + 0.01 * kCostProbe) + hits * kCostCompare);
                 else       // start keys: one probe per verified start
                   cost += cpb * kCostCand + pm * (kCostStart + fp * kCostProbe + hits * kCostCompare);
                 if (cost < best.cost * 0.999) {
@@ -516,6 +521,43 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         }
       }
     }
+    // direct q = 16 stream kernel: no staging, the table takes the smem
+    if (rq.table_bits >= 0 && !sp.overlapping && m >= 31 && (rq.q == 0 || rq.q == 16) &&
+        rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0) {
+      const unsigned q = 16;
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+      ScanPlan z{};
+      const size_t fixed = direct_smem(z, warps) + 1024;
+      const size_t room = rq.smem_limit > fixed ? rq.smem_limit - fixed : 0;
+      const uint32_t blocks = static_cast<uint32_t>(std::min<size_t>(room / 8, 1u << 22));
+      const double universe = std::pow(static_cast<double>(sigma_obs), 16.0);
+      const double adm = keys * q;
+      const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
+      const double exact = universe > 1e15 ? 0.0 : distinct / universe;
+      const double hits = key_hits(adm, sigma_obs, static_cast<unsigned>(std::min<size_t>(16, m - q + 1)));
+      for (unsigned H = 2; H <= kMaxProbes && blocks > 0; ++H) {
+        if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
+        const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / (64.0 * blocks));
+        const double p = exact + (1.0 - exact) * std::pow(fill, static_cast<double>(H));
+        const double cpb = p / q;
+        const double cost = (kCostSample + H * kCostProbeBit) / q +
+                            cpb * (kCostCand + kCostScreen + 0.01 * kCostProbe + hits * kCostCompare);
+        if (cost < best.cost * 0.999) {
+          best.cost = cost;
+          best.q = q;
+          best.k = 1;
+          best.mp = 1;
+          best.tb = 0;
+          best.H = H;
+          best.pf = 0;
+          best.chunk = kChunkTarget;
+          best.va = false;
+          best.cpb = cpb;
+          best.direct = 1;
+          best.blocks = blocks;
+        }
+      }
+    }
     if (best.va) {
       sp.q = 1;
       sp.k = 1;
@@ -530,6 +572,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.table_bits = best.tb;
       sp.entries = 1ull << best.tb;
       sp.probes = best.H;
+      sp.blocks = best.H > 1 ? (best.direct ? best.blocks : static_cast<uint32_t>((1ull << best.tb) / 64)) : 0;
+      sp.direct = best.direct;
     }
     sp.pf_bits = best.pf;
     P->chunk_target = best.chunk;
@@ -577,6 +621,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.pf_bits = pf;
   } else {
     sp.table_in_smem = sp.verify_all ? 0 : 1;
+    if (sp.direct) P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
@@ -593,7 +638,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.bucket_bits = bb;
   }
   // oversized rings (long patterns, wide windows): fewer warps per CTA
-  while (plan_smem(*P) > rq.smem_limit && P->nwarps > 1) P->nwarps /= 2;
+  while (!sp.direct && plan_smem(*P) > rq.smem_limit && P->nwarps > 1) P->nwarps /= 2;
   const size_t total = plan_smem(*P);
   if (total > rq.smem_limit) {
     *err = "plan needs " + std::to_string(total) + " bytes of shared memory (limit " +
@@ -604,6 +649,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
 }
 
 size_t plan_smem(const Plan& p) {
+  if (p.sp.direct) return direct_smem(p.sp, p.nwarps);
   return smem_layout(p.sp, p.slot_bytes, p.ring, p.nwarps).total;
 }
 
@@ -619,8 +665,8 @@ static inline uint32_t gram_index_host(const Plan& P, const uint8_t* g) {
 }
 
 // Entries of a gram under multi-probe hashing (probes >= 2).
-static inline uint32_t probe_entry(const ScanPlan& sp, uint32_t h, unsigned i) {
-  return (probe_block(h, sp.table_bits) << 5) | probe_bit(h, i);
+static inline uint64_t probe_entry(const ScanPlan& sp, uint32_t h, unsigned i) {
+  return static_cast<uint64_t>(bloom_block(h, sp.blocks)) * 64 + bloom_bit(bloom_mix(h), i);
 }
 
 static inline void clear_bit(const Plan& P, std::vector<uint8_t>* t, uint64_t idx, unsigned b) {

@@ -73,6 +73,7 @@ struct PlanRequest {
   int table_bits = 0;        // hashed: 0 auto, -1 verify-all
   int word_bits = 0;
   int tile_bytes = 0, warps = 0, stages = 0;  // tile_bytes: chunk bytes target; stages: ring
+  int probes = 0;            // hashed: 0 auto
   size_t smem_limit = 232448;  // sm_100 max dynamic shared memory per CTA
 };
 

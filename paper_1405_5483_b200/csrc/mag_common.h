@@ -56,13 +56,18 @@ MAG_HD uint32_t gram_slot(uint32_t h, unsigned table_bits) {
   return table_bits ? (h >> (32 - table_bits)) : 0u;
 }
 
-// Multi-probe hashed grams (1-bit entries, probes >= 2): a gram owns
-// `probes` entries inside one 32-entry block of the table — block
-// h >> (37 - table_bits), entry bits taken from a second mix of h — and is
-// admitted only where all of them are admitted.  An intersection of hashed
-// q-gram alphabets: still never rejects a gram a pattern contributed.
-MAG_HD uint32_t probe_block(uint32_t h, unsigned table_bits) { return h >> (37 - table_bits); }
-MAG_HD uint32_t probe_bit(uint32_t h, unsigned i) { return ((h * 0x9E3779B1u) >> (27 - 5 * i)) & 31u; }
+// Multi-probe hashed grams (1-bit entries, probes >= 2): the table is
+// `blocks` 64-entry blocks; a gram owns `probes` entries of block
+// (h * blocks) >> 32, at bits taken from a 64-bit mix of h, and is admitted
+// only where all of them are admitted — an intersection of hashed q-gram
+// alphabets (a blocked Bloom filter), which still never rejects a gram a
+// pattern contributed.  Entry index = block * 64 + bit.
+constexpr unsigned kMaxProbes = 8;
+MAG_HD uint32_t bloom_block(uint32_t h, uint32_t blocks) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(h) * blocks) >> 32);
+}
+MAG_HD uint64_t bloom_mix(uint32_t h) { return static_cast<uint64_t>(h) * 0x9E3779B97F4A7C15ull; }
+MAG_HD uint32_t bloom_bit(uint64_t g, unsigned i) { return static_cast<uint32_t>(g >> (58 - 6 * i)) & 63u; }
 
 // Verification key: the first v = min(m, 16) bytes of a start, read as four
 // little-endian words (bytes past v zeroed), mixed.  Top bits index the
@@ -103,7 +108,9 @@ struct ScanPlan {
   uint32_t q, k, m_prime;
   uint32_t sigma_prime;
   uint32_t table_bits;    // hashed: log2(entries)
-  uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..4)
+  uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..kMaxProbes)
+  uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
+  int direct;             // q = 16 stream kernel (register prefetch, no staging)
   uint32_t entry_log2;    // log2(bits per mask entry), 0..6
   uint64_t entries;       // number of mask entries
   uint64_t table_bytes;   // packed table size (multiple of 16)
@@ -152,6 +159,15 @@ struct SmemLayout {
   size_t table, pf, map, slots, info, queue, probe, hits, bars, total;
 };
 
+// Direct (q = 16) kernel: resident table, per-warp probe queue, and a ring
+// of kDirectDepth 1 KiB step buffers (+ mbarriers) per warp.
+constexpr int kDirectDepth = 4;
+constexpr int kDirectStep = 64;  // samples per step (1 KiB of text)
+MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
+  return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
+         size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * 8 + 64;
+}
+
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,
                               uint32_t nwarps) {
   SmemLayout L;
@@ -169,7 +185,7 @@ MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t r
   L.queue = o;
   o += align16(size_t(nwarps) * kQueueCap * 4);
   L.probe = o;
-  o += align16(size_t(nwarps) * kProbeCap * 8);
+  o += align16(size_t(nwarps) * kProbeCap * 12);  // {key, pos} + prefetched screen word
   L.hits = o;
   o += align16(size_t(nwarps) * kHitWords * 4);
   L.bars = o;

@@ -65,6 +65,12 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -98,6 +104,17 @@ __device__ __forceinline__ uint32_t popc_e(E v) {
     return __popcll(static_cast<unsigned long long>(v));
   else
     return __popc(static_cast<uint32_t>(v));
+}
+
+__device__ __forceinline__ bool bloom_admits(const unsigned long long* tab, const ScanPlan& P,
+                                             uint32_t h) {
+  const unsigned long long blk = tab[bloom_block(h, P.blocks)];
+  const uint64_t g = bloom_mix(h);
+  unsigned long long m = 0;
+#pragma unroll
+  for (unsigned i = 0; i < kMaxProbes; ++i)
+    if (i < P.probes) m |= blk >> bloom_bit(g, i);
+  return !(m & 1ull);
 }
 
 // Gram formation modes for the kernel template.
@@ -139,6 +156,7 @@ struct Scanner {
   uint32_t fill;                // matches written for the current slice
   // window keys awaiting the L2 screen: {key, start position - pbase}
   uint2* pq;
+  uint32_t* pqw;                // screen words, fetched asynchronously (cp.async)
   uint32_t pqn;
   uint32_t* hbm;                // hit bitmap of the chunk (k = 1 strided)
   uint32_t cands32;             // candidates since the last fold into `cands`
@@ -174,6 +192,8 @@ struct Scanner {
     mybars = S.bars + static_cast<size_t>(w) * A.ring;
     queue = S.queue + static_cast<size_t>(w) * kQueueCap;
     pq = S.probe + static_cast<size_t>(w) * kProbeCap;
+    pqw = reinterpret_cast<uint32_t*>(S.probe + static_cast<size_t>(A.nwarps) * kProbeCap) +
+          static_cast<size_t>(w) * kProbeCap;
     hbm = S.hits + static_cast<size_t>(w) * kHitWords;
     cands32 = 0;
     ld_slice = 0;
@@ -271,6 +291,12 @@ struct Scanner {
     }
   }
 
+  // Multi-probe membership (probes >= 2): all probed entries of the gram's
+  // 64-entry block admit (bit 0).
+  __device__ __forceinline__ bool bloom_test(uint32_t h) const {
+    return bloom_admits(static_cast<const unsigned long long*>(S.table), A.plan, h);
+  }
+
   // Mask of the gram at slot offset rel, read by sample t (absolute; used
   // for SMAG's code array).
   __device__ __forceinline__ E gram_mask(uint32_t rel, unsigned long long t) const {
@@ -306,16 +332,7 @@ struct Scanner {
       }
       const uint32_t h = hash_gram_words(x[0], x[1], x[2], x[3]);
       if constexpr (CMP == 1 && CK == 1 && sizeof(E) == 4 && TSMEM) {
-        if (P.probes > 1) {
-          // multi-probe: one block word, all probed entries must admit
-          const uint32_t blk = static_cast<const uint32_t*>(S.table)[probe_block(h, P.table_bits)];
-          const uint32_t g = h * 0x9E3779B1u;
-          uint32_t m = blk >> (g >> 27);
-          m |= blk >> ((g >> 22) & 31u);
-          if (P.probes > 2) m |= blk >> ((g >> 17) & 31u);
-          if (P.probes > 3) m |= blk >> ((g >> 12) & 31u);
-          return static_cast<E>(m & 1u);
-        }
+        if (P.probes > 1) return static_cast<E>(bloom_test(h) ? 0u : 1u);
       }
       return table_entry(h >> (32 - P.table_bits));
     } else {
@@ -450,8 +467,13 @@ struct Scanner {
   // = text order); the four L2 bitmap loads are independent, so one round
   // trip covers 128 windows.  Survivors walk their bucket.
   __device__ void flush_pq() {
-    __syncwarp();
     const uint32_t lb = A.plan.l2_bits;
+    if (A.plan.diag & 2) {  // diagnostics: keys only, no screen / probes
+      pqn = 0;
+      return;
+    }
+    cp_async_wait_all();
+    __syncwarp();
     for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
       const uint32_t i0 = b0 + 4 * lane;
       uint2 e[4];
@@ -459,8 +481,7 @@ struct Scanner {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
-        w[j] = 1u;
-        if (lb && e[j].y != 0xffffffffu) w[j] = __ldg(A.l2map + ((e[j].x >> (32 - lb)) >> 5));
+        w[j] = (lb && i0 + j < pqn) ? pqw[i0 + j] : ~0u;
       }
       uint32_t cnt[4], c = 0;
 #pragma unroll
@@ -481,6 +502,31 @@ struct Scanner {
     }
     pqn = 0;
     __syncwarp();
+  }
+
+  // One candidate window per lane (super position ss, lane order = text
+  // order): its key, read now from the staged chunk, joins the probe queue.
+  // Windows whose key would run past the text cannot match.
+  __device__ __forceinline__ void push_window(bool live, long long ss) {
+    const uint32_t v = A.plan.wkey_len;
+    const unsigned long long a0 = static_cast<unsigned long long>(ss) * A.plan.q;
+    bool ok = live && a0 + v <= A.n;
+    uint32_t key = 0;
+    if (ok) {
+      key = key_at(static_cast<uint32_t>(a0 - src), v);
+      ok = prefilter_pass(key);
+    }
+    const unsigned bal = __ballot_sync(kFull, ok);
+    if (!bal) return;
+    if (pqn + __popc(bal) > kProbeCap) flush_pq();
+    if (ok) {
+      const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
+      pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
+      const uint32_t lb = A.plan.l2_bits;
+      if (lb && !(A.plan.diag & 2)) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));  // lands before flush_pq
+    }
+    __syncwarp();
+    pqn += __popc(bal);
   }
 
   // Queued candidate windows -> keys (read from the staged chunk now) in the
@@ -504,7 +550,12 @@ struct Scanner {
       const unsigned bal = __ballot_sync(kFull, ok);
       if (!bal) continue;
       if (pqn + __popc(bal) > kProbeCap) flush_pq();
-      if (ok) pq[pqn + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
+      if (ok) {
+        const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
+        pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
+        const uint32_t lb = A.plan.l2_bits;
+        if (lb) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));
+      }
       __syncwarp();
       pqn += __popc(bal);
     }
@@ -519,6 +570,10 @@ struct Scanner {
       drain_windows(qlen, ss_ref);
       return;
     }
+    drain_starts(qlen, ss_ref);
+  }
+
+  __device__ void drain_starts(uint32_t qlen, long long ss_ref) {
     __syncwarp();
     const uint32_t pairs = qlen * W;
     for (uint32_t p0 = 0; p0 < pairs; p0 += 32) {
@@ -589,6 +644,51 @@ struct Scanner {
     }
   }
 
+  // q = 16, m' = k = 1, 16-byte window keys (the cfg2/cfg4 plan shape): a
+  // candidate's window key is the very gram the filter just hashed, so hit
+  // lanes hash their key from the registers and append it to the probe queue
+  // in place — no bitmap, no expansion, no second read of the slot.
+  __device__ __forceinline__ void push_inline(bool hit, uint32_t key, unsigned long long a0) {
+    const unsigned bal = __ballot_sync(kFull, hit);
+    if (!bal) return;
+    cands32 += hit ? 1u : 0u;
+    if (pqn + __popc(bal) > kProbeCap) flush_pq();
+    if (hit) {
+      const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
+      pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
+      const uint32_t lb = A.plan.l2_bits;
+      if (lb) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));
+    }
+    __syncwarp();
+    pqn += __popc(bal);
+  }
+
+  __device__ void fused_window_loop(const SlotInfo& in, int g0, int nsamp) {
+    const ScanPlan& P = A.plan;
+    const uint32_t tb = P.table_bits;
+    const uint32_t* tab = static_cast<const uint32_t*>(S.table);
+    const unsigned long long gbase = src + static_cast<unsigned long long>(g0);  // absolute byte of sample 0
+    for (int base = 0; base < nsamp; base += 64) {
+      uint32_t key[2];
+      bool hit[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int t = base + 32 * h + lane;
+        const uint4 v = *reinterpret_cast<const uint4*>(sw + ((g0 + 16 * t) >> 2));
+        const uint32_t gh = hash_gram_words(v.x, v.y, v.z, v.w);
+        if (P.probes > 1) {
+          hit[h] = bloom_test(gh);
+        } else {
+          const uint32_t idx = gh >> (32 - tb);
+          hit[h] = !((tab[idx >> 5] >> (idx & 31u)) & 1u);
+        }
+        key[h] = key_words(v.x, v.y, v.z, v.w);
+      }
+      push_inline(hit[0], key[0], gbase + 16ull * (base + lane));
+      push_inline(hit[1], key[1], gbase + 16ull * (base + 32 + lane));
+    }
+  }
+
   // k = 1 strided chunk: the filter only records hit ballots (one bit per
   // sample, in a per-chunk bitmap); the bitmap is expanded into candidate
   // windows once at the end of the chunk.
@@ -606,6 +706,12 @@ struct Scanner {
     const int nwords = (nsamp + 31) >> 5;
     if (lane < nwords) hbm[lane] = 0u;
     __syncwarp();
+    if constexpr (GM == kKHashed && A4 && QW == 4 && CMP == 1 && CK == 1) {
+      if ((nsamp & 63) == 0 && thit == 0 && P.window_key && P.wkey_len == 16 && !(P.diag & 1)) {
+        fused_window_loop(in, g0, nsamp);
+        return;
+      }
+    }
     if (CMP == 1 && (nsamp & 63) == 0 && thit == 0) {
       // interior m' = 1 chunk: every lane valid, hits are ~mask & 1
       for (int base = 0; base < nsamp; base += 64) {
@@ -667,19 +773,33 @@ struct Scanner {
     const uint32_t excl = warp_excl_scan(cnt, lane);
     const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
     if (P.diag & 1) return;
-    for (uint32_t r0 = 0; r0 < total; r0 += kQueueCap) {
-      if (cnt && excl < r0 + kQueueCap && excl + cnt > r0) {
-        uint32_t wv = word, rank = excl;
-        while (wv) {
-          const int b = __ffs(wv) - 1;
-          wv &= wv - 1;
-          if (rank >= r0 && rank < r0 + kQueueCap) queue[rank - r0] = static_cast<uint32_t>(32 * lane + b);
-          ++rank;
-        }
+    // lane r takes the candidate of rank r: its word is found by binary
+    // search over the word prefix counts, its bit with __fns
+    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+      const uint32_t rank = r0 + lane;
+      int w = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int c = w + step;
+        const uint32_t e = __shfl_sync(kFull, excl, c & 31);
+        if (c < nwords && e <= rank) w = c;
       }
-      __syncwarp();
-      const uint32_t qn = total - r0 < static_cast<uint32_t>(kQueueCap) ? total - r0 : kQueueCap;
-      drain(qn, ss_ref);
+      const uint32_t ww = __shfl_sync(kFull, word, w);
+      const uint32_t ew = __shfl_sync(kFull, excl, w);
+      const bool live = rank < total;
+      const int t_rel = 32 * w + static_cast<int>(__fns(ww, 0, static_cast<int>(rank - ew) + 1));
+      if (P.diag & 4) {  // diagnostics: expansion only
+        if (live && t_rel < 0) cands32 += 1;
+        continue;
+      }
+      if (P.window_key) {
+        push_window(live, ss_ref + t_rel);
+      } else {
+        const uint32_t bal = __ballot_sync(kFull, live);
+        if (live) queue[lane] = static_cast<uint32_t>(t_rel);
+        __syncwarp();
+        drain_starts(__popc(bal), ss_ref);
+      }
     }
   }
 
@@ -830,6 +950,304 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
   }
   Scanner<GM, E, TSMEM, QW, CMP, CK, A4> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
   sc.run();
+}
+
+// ============================================================ direct kernel
+// q = 16, k = m' = 1 hashed plans (the DNA r = 10k shape): sample t is the
+// aligned 16-byte word text[16t, 16t + 16), so warps stream samples straight
+// from HBM with coalesced 16-byte loads, kDirectDepth steps of 64 samples
+// prefetched in registers — no shared-memory staging at all, which leaves
+// the whole shared memory to a multi-probe filter table.  A hit's window key
+// is the same 16 bytes (hashed from the registers); keys queue per warp and
+// are screened against the L2 bitmap, survivors walk their bucket and are
+// compared against the text in global memory.  Output: per-slice ordered
+// staging, exactly as the staged kernel.
+__device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid,
+                                           uint32_t len) {
+  const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
+  const uint8_t* t = A.text + a;
+  for (uint32_t i = 0; i < len; ++i)
+    if (__ldg(t + i) != __ldg(p + i)) return false;
+  return true;
+}
+
+// Window-key bucket walk (see Scanner::probe_window).
+__device__ uint32_t window_probe(const ScanArgs& A, unsigned long long a0, uint32_t key,
+                                 uint64_t* dst, uint32_t idx) {
+  const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
+  const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
+  uint32_t c = 0;
+  for (uint32_t e = lo; e < hi; ++e) {
+    const uint2 ent = __ldg(A.bucket_entries + e);
+    if (ent.x != key) continue;
+    const uint32_t s = ent.y >> kPidBits, pid = ent.y & ((1u << kPidBits) - 1u);
+    if (s > a0) continue;
+    const unsigned long long a = a0 - s;
+    const uint32_t len = __ldg(A.pat_len + pid);
+    if (a + len > A.n || !equal_text(A, a, pid, len)) continue;
+    if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, pid);
+    ++c;
+  }
+  return c;
+}
+
+struct DirectIter {
+  unsigned long long slice, t;  // owning slice, first sample of the step
+  uint32_t lim;                 // valid samples in the step (<= 64)
+  uint32_t flags;               // 1 first step of its slice, 2 last, 4 valid
+};
+
+// Multi-probe membership on a 64-entry block given as two words.
+template <int H>
+__device__ __forceinline__ bool bloom_admits_w(uint32_t lo, uint32_t hi, uint32_t h) {
+  const uint64_t g = bloom_mix(h);
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const uint32_t b = bloom_bit(g, i);
+    m |= ((b & 32u) ? hi : lo) >> (b & 31u);
+  }
+  return !(m & 1u);
+}
+
+template <int H>
+struct DirectScanner {
+  const ScanArgs& A;
+  const int lane;
+  const void* table;
+  uint2* pq;
+  uint4* slots;    // [kDirectDepth][kDirectStep] staged samples
+  uint64_t* bars;  // [kDirectDepth]
+  uint32_t pqn, fill, cands32;
+  unsigned long long pbase;
+  uint64_t* out;
+  uint32_t km[4];  // window-key word masks
+  // slice stream (warp-uniform)
+  unsigned long long s_slice, s_t;
+  uint32_t s_left;  // samples left in the slice
+  bool s_done, s_first;
+
+  __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint4* sl, uint64_t* b, int l)
+      : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), pqn(0), fill(0), cands32(0), pbase(0),
+        out(nullptr) {
+    for (int i = 0; i < 4; ++i) km[i] = key_word_mask(A.plan.wkey_len, i);
+    s_slice = s_t = 0;
+    s_left = 0;
+    s_done = false;
+    s_first = false;
+  }
+
+  __device__ __forceinline__ void next(DirectIter& d) {
+    while (!s_done && s_left == 0) {
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(A.ticket, 1ull);
+      x = __shfl_sync(kFull, x, 0) + A.slice_begin;
+      if (x >= A.slice_end) {
+        s_done = true;
+        break;
+      }
+      s_slice = x;
+      s_t = x * A.slice_samples;
+      const unsigned long long end = s_t + A.slice_samples < A.samples ? s_t + A.slice_samples : A.samples;
+      s_left = end > s_t ? static_cast<uint32_t>(end - s_t) : 0u;
+      s_first = true;
+      if (s_left == 0 && lane == 0) A.slice_count[x] = 0;
+    }
+    if (s_done) {
+      d.flags = 0;
+      return;
+    }
+    d.slice = s_slice;
+    d.t = s_t;
+    d.lim = s_left < 64u ? s_left : 64u;
+    d.flags = 4u | (s_first ? 1u : 0u) | (s_left <= 64u ? 2u : 0u);
+    s_first = false;
+    s_t += d.lim;
+    s_left -= d.lim;
+  }
+
+  // Stage step d into ring slot j (TMA bulk copy, completion on bar[j]).
+  __device__ __forceinline__ void issue(const DirectIter& d, int j) {
+    if (lane == 0) {
+      const uint32_t bytes = 16u * d.lim;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bars + j, bytes);
+      tma_load_1d(slots + j * kDirectStep, A.text + 16 * d.t, bytes, bars + j);
+    }
+  }
+
+  __device__ __forceinline__ bool admits(uint32_t h) const {
+    if constexpr (H > 1) {
+      const uint2 blk = static_cast<const uint2*>(table)[bloom_block(h, A.plan.blocks)];
+      return bloom_admits_w<H>(blk.x, blk.y, h);
+    } else {
+      const uint32_t idx = h >> (32 - A.plan.table_bits);
+      return !((static_cast<const uint32_t*>(table)[idx >> 5] >> (idx & 31u)) & 1u);
+    }
+  }
+
+  __device__ void flush() {
+    __syncwarp();
+    const uint32_t lb = A.plan.l2_bits;
+    for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
+      const uint32_t i0 = b0 + 4 * lane;
+      uint2 e[4];
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
+        w[j] = ~0u;
+        if (lb && e[j].y != 0xffffffffu) w[j] = __ldg(A.l2map + ((e[j].x >> (32 - lb)) >> 5));
+      }
+      uint32_t cnt[4], c = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        cnt[j] = 0;
+        const bool live = e[j].y != 0xffffffffu && (!lb || ((w[j] >> ((e[j].x >> (32 - lb)) & 31u)) & 1u));
+        if (live) cnt[j] = window_probe(A, pbase + e[j].y, e[j].x, nullptr, 0);
+        c += cnt[j];
+      }
+      if (!__any_sync(kFull, c != 0)) continue;
+      const uint32_t excl = warp_excl_scan(c, lane);
+      const uint32_t total = __shfl_sync(kFull, excl + c, 31);
+      uint32_t at = fill + excl;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (cnt[j]) at += window_probe(A, pbase + e[j].y, e[j].x, out, at);
+      fill += total;
+    }
+    pqn = 0;
+    __syncwarp();
+  }
+
+  // hit lanes queue {window key, 16 * sample - pbase}
+  __device__ __forceinline__ void push(bool hit, uint32_t key, uint32_t pos) {
+    const unsigned bal = __ballot_sync(kFull, hit);
+    if (!bal) return;
+    cands32 += hit ? 1u : 0u;
+    if (pqn + __popc(bal) > kProbeCap) flush();
+    if (hit) pq[pqn + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key, pos);
+    __syncwarp();
+    pqn += __popc(bal);
+  }
+
+  __device__ __forceinline__ void half(const uint4& v, bool valid, uint32_t pos) {
+    const uint32_t h = hash_gram_words(v.x, v.y, v.z, v.w);
+    const bool hit = valid && admits(h);
+    const uint32_t key = key_words(v.x & km[0], v.y & km[1], v.z & km[2], v.w & km[3]);
+    push(hit, key, pos);
+  }
+
+  __device__ __forceinline__ void process(const DirectIter& d, const uint4& a, const uint4& b) {
+    if (d.flags & 1u) {
+      fill = 0;
+      pqn = 0;
+      pbase = 16 * d.t;
+      out = A.staging + static_cast<size_t>(d.slice) * A.slice_cap;
+    }
+    const uint32_t pos0 = static_cast<uint32_t>(16 * d.t - pbase) + 16u * lane;
+    half(a, static_cast<uint32_t>(lane) < d.lim, pos0);
+    half(b, static_cast<uint32_t>(lane) + 32 < d.lim, pos0 + 512u);
+    if (d.flags & 2u) {
+      if (pqn) flush();
+      if (lane == 0) A.slice_count[d.slice] = fill;
+    }
+  }
+
+  __device__ void run() {
+    DirectIter d[kDirectDepth];
+#pragma unroll
+    for (int j = 0; j < kDirectDepth; ++j) {
+      next(d[j]);
+      if (d[j].flags & 4u) issue(d[j], j);
+    }
+    uint32_t phase = 0;  // bit j: parity of slot j's next completion
+    bool more = true;
+    while (more) {
+#pragma unroll
+      for (int j = 0; j < kDirectDepth; ++j) {
+        if (!(d[j].flags & 4u)) {
+          more = false;
+          break;
+        }
+        mbar_wait(bars + j, (phase >> j) & 1u);
+        phase ^= 1u << j;
+        const uint4 a = slots[j * kDirectStep + lane];
+        const uint4 b = slots[j * kDirectStep + 32 + lane];
+        const DirectIter cur = d[j];
+        __syncwarp();
+        next(d[j]);
+        if (d[j].flags & 4u) issue(d[j], j);  // refill the slot just read
+        process(cur, a, b);
+      }
+    }
+    unsigned long long c = cands32;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0 && c) atomicAdd(A.counters + 1, c);
+  }
+};
+
+template <int H>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const size_t tbytes = align16(A.plan.table_bytes);
+  {
+    const uint4* src = static_cast<const uint4*>(A.table);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (size_t i = threadIdx.x; i < tbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  uint8_t* p = smem + tbytes;
+  uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kProbeCap;
+  p += align16(size_t(nw) * kProbeCap * 8);
+  uint4* slots = reinterpret_cast<uint4*>(p) + static_cast<size_t>(warp) * kDirectDepth * kDirectStep;
+  p += size_t(nw) * kDirectDepth * kDirectStep * 16;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kDirectDepth;
+  if ((threadIdx.x & 31) == 0) {
+    for (int j = 0; j < kDirectDepth; ++j) mbar_init(bars + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  DirectScanner<H> ds(A, smem, pq, slots, bars, threadIdx.x & 31);
+  ds.run();
+}
+
+template <int H>
+cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
+  static int configured = -1;
+  if (configured != static_cast<int>(smem)) {
+    cudaError_t e = cudaFuncSetAttribute(mag_direct_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = static_cast<int>(smem);
+  }
+  mag_direct_kernel<H><<<grid, a.nwarps * 32, smem, stream>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
+  const size_t smem = direct_smem(a.plan, a.nwarps);
+  switch (a.plan.probes) {
+    case 1: return launch_direct_h<1>(a, stream, grid, smem);
+    case 2: return launch_direct_h<2>(a, stream, grid, smem);
+    case 3: return launch_direct_h<3>(a, stream, grid, smem);
+    case 4: return launch_direct_h<4>(a, stream, grid, smem);
+    case 5: return launch_direct_h<5>(a, stream, grid, smem);
+    case 6: return launch_direct_h<6>(a, stream, grid, smem);
+    case 7: return launch_direct_h<7>(a, stream, grid, smem);
+    default: return launch_direct_h<8>(a, stream, grid, smem);
+  }
 }
 
 // Gather: block b owns slices [b*per, (b+1)*per); its output offset is the
@@ -983,6 +1401,7 @@ LaunchShape scan_shape(const ScanArgs& a) {
 }
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
+  if (a.plan.direct) return launch_direct(a, stream, grid);
   const size_t smem = smem_layout(a.plan, a.slot_bytes, a.ring, a.nwarps).total;
   if (a.plan.smag) return launch_e<kKCodes>(a, stream, grid, smem);
   if (a.plan.gram_mode == kGramHashed) return launch_e<kKHashed>(a, stream, grid, smem);

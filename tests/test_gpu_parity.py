@@ -121,7 +121,8 @@ def test_hashed_counters_match_port(mag, ref, port):
             assert met.candidates == met.filter_reads
             continue
         P = port.params(variant=0 if variant == "mag" else 2, gram_mode=1, q=pl["q"], k=pl["k"],
-                        table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"])
+                        table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
+                        blocks=pl["blocks"])
         o, p, reads, cands = port.search(text, pats, P)
         assert (met.filter_reads, met.candidates) == (reads, cands), (it, pl)
 
