@@ -535,9 +535,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
       const double exact = universe > 1e15 ? 0.0 : distinct / universe;
       const double hits = key_hits(adm, sigma_obs, static_cast<unsigned>(std::min<size_t>(16, m - q + 1)));
-      for (unsigned H = 2; H <= kMaxProbes && blocks > 0; ++H) {
+      // single probe: largest power-of-two table that fits
+      unsigned tb1 = 6;
+      while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room) ++tb1;
+      for (unsigned H = 1; H <= kMaxProbes && blocks > 0; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
-        const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / (64.0 * blocks));
+        const double bits = H == 1 ? std::ldexp(1.0, static_cast<int>(tb1)) : 64.0 * blocks;
+        const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / bits);
         const double p = exact + (1.0 - exact) * std::pow(fill, static_cast<double>(H));
         const double cpb = p / q;
         const double cost = (kCostSample + H * kCostProbeBit) / q +
@@ -554,7 +558,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.va = false;
           best.cpb = cpb;
           best.direct = 1;
-          best.blocks = blocks;
+          best.blocks = H > 1 ? blocks : 0;
+          best.tb = H > 1 ? 0 : tb1;
         }
       }
     }
@@ -625,6 +630,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
+  sp.key_gram = sp.direct && sp.wkey_len == 16;
   sp.l2_bits = 0;
   if (sp.window_key) {  // ~128 bits per key: ~0.8% of screened keys walk a bucket
     unsigned lb = 16;
@@ -740,7 +746,8 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
     ents.reserve(r * sp.q);
     for (int s = static_cast<int>(sp.q) - 1; s >= 0; --s)
       for (size_t i = 0; i < r; ++i)
-        ents.push_back({key_bytes(pd.pattern(i) + s, sp.wkey_len),
+        ents.push_back({sp.key_gram ? hash_gram_bytes(pd.pattern(i) + s, 16)
+                                    : key_bytes(pd.pattern(i) + s, sp.wkey_len),
                         static_cast<uint32_t>(i) | (static_cast<uint32_t>(s) << kPidBits)});
   } else {
     ents.reserve(r);
@@ -762,7 +769,7 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   pt->l2map.assign(sp.l2_bits ? std::max<size_t>(4, (size_t(1) << sp.l2_bits) / 32) : 4, 0);
   if (sp.l2_bits) {
     for (const Ent& e : ents) {
-      const uint32_t b = e.key >> (32 - sp.l2_bits);
+      const uint32_t b = screen_bit(e.key, sp.l2_bits);
       pt->l2map[b >> 5] |= 1u << (b & 31);
     }
   }

@@ -91,6 +91,15 @@ MAG_HD uint32_t key_bytes(const uint8_t* p, unsigned v) {
   return key_words(x[0], x[1], x[2], x[3]);
 }
 
+// L2 screen bit of a window key: re-mixed so it is independent of the
+// filter table slot (which uses the top bits of the same gram hash).
+MAG_HD uint32_t screen_bit(uint32_t key, unsigned l2_bits) {
+  uint32_t x = key * 0x7FEB352Du;
+  x ^= x >> 15;
+  x *= 0x846CA68Bu;
+  return x >> (32 - l2_bits);
+}
+
 // Byte masks of the v-byte key per word.
 MAG_HD uint32_t key_word_mask(unsigned v, unsigned word) {
   if (v >= 4 * (word + 1)) return 0xffffffffu;
@@ -124,8 +133,11 @@ struct ScanPlan {
   // each hit naming the start q*ss - s directly.
   int window_key;
   uint32_t wkey_len;
+  // key_gram: window keys are 16 bytes hashed with hash_gram_words (the
+  // filter's own gram hash: q = 16 direct plans reuse one hash per sample)
+  int key_gram;
   // Window keys are screened by an L2-resident bitmap of 2^l2_bits bits
-  // (bit = key >> (32 - l2_bits)) before any bucket walk; 0 = no bitmap.
+  // (bit = screen_bit(key)) before any bucket walk; 0 = no bitmap.
   uint32_t l2_bits;
   // diagnostics only (MAG_B200_DIAG env): 1 = skip candidate verification
   int diag;

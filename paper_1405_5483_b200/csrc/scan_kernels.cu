@@ -71,6 +71,21 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
+// Text is read once: stream it through L2 with an evict-first policy so it
+// does not push the pattern tables and the screen bitmap out of L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_1d_stream(void* dst, const void* src, uint32_t bytes,
+                                                   uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -116,6 +131,10 @@ __device__ __forceinline__ bool bloom_admits(const unsigned long long* tab, cons
     if (i < P.probes) m |= blk >> bloom_bit(g, i);
   return !(m & 1ull);
 }
+
+__device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len);
+__device__ void flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned long long pbase,
+                            uint64_t* out, uint32_t& fill, int lane);
 
 // Gram formation modes for the kernel template.
 enum KGram : int { kKExact = 0, kKHashed = 1, kKCodes = 2 };
@@ -268,7 +287,7 @@ struct Scanner {
       in.flags = (t0 == ld_slice * A.slice_samples ? 1u : 0u) | (t0 + nsamp == ld_tend ? 2u : 0u);
       fence_proxy_async();
       mbar_arrive_expect_tx(mybars + slot, bulk);
-      if (bulk) tma_load_1d(dst, A.text + lo, bulk, mybars + slot);
+      if (bulk) tma_load_1d_stream(dst, A.text + lo, bulk, mybars + slot, policy_evict_first());
     }
     __syncwarp();
     ld_t = t0 + nsamp;
@@ -437,11 +456,7 @@ struct Scanner {
   // (true matches and 32-bit key collisions) and compare against the text in
   // global memory, so queued keys outlive the staged chunk.
   __device__ bool equal_global(unsigned long long a, uint32_t pid, uint32_t len) const {
-    const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
-    const uint8_t* t = A.text + a;
-    for (uint32_t i = 0; i < len; ++i)
-      if (__ldg(t + i) != __ldg(p + i)) return false;
-    return true;
+    return equal_text(A, a, pid, len);
   }
 
   __device__ uint32_t probe_window(unsigned long long a0, uint32_t key, uint64_t* dst,
@@ -467,41 +482,9 @@ struct Scanner {
   // = text order); the four L2 bitmap loads are independent, so one round
   // trip covers 128 windows.  Survivors walk their bucket.
   __device__ void flush_pq() {
-    const uint32_t lb = A.plan.l2_bits;
-    if (A.plan.diag & 2) {  // diagnostics: keys only, no screen / probes
-      pqn = 0;
-      return;
-    }
     cp_async_wait_all();
-    __syncwarp();
-    for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
-      const uint32_t i0 = b0 + 4 * lane;
-      uint2 e[4];
-      uint32_t w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
-        w[j] = (lb && i0 + j < pqn) ? pqw[i0 + j] : ~0u;
-      }
-      uint32_t cnt[4], c = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        cnt[j] = 0;
-        const bool live = e[j].y != 0xffffffffu && (!lb || ((w[j] >> ((e[j].x >> (32 - lb)) & 31u)) & 1u));
-        if (live) cnt[j] = probe_window(pbase + e[j].y, e[j].x, nullptr, 0);
-        c += cnt[j];
-      }
-      if (!__any_sync(kFull, c != 0)) continue;
-      const uint32_t excl = warp_excl_scan(c, lane);
-      const uint32_t total = __shfl_sync(kFull, excl + c, 31);
-      uint32_t at = fill + excl;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (cnt[j]) at += probe_window(pbase + e[j].y, e[j].x, out, at);
-      fill += total;
-    }
+    if (!(A.plan.diag & 2)) flush_queue(A, pq, pqn, pbase, out, fill, lane);
     pqn = 0;
-    __syncwarp();
   }
 
   // One candidate window per lane (super position ss, lane order = text
@@ -523,7 +506,6 @@ struct Scanner {
       const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
       pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
       const uint32_t lb = A.plan.l2_bits;
-      if (lb && !(A.plan.diag & 2)) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));  // lands before flush_pq
     }
     __syncwarp();
     pqn += __popc(bal);
@@ -553,8 +535,7 @@ struct Scanner {
       if (ok) {
         const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
         pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
-        const uint32_t lb = A.plan.l2_bits;
-        if (lb) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));
+
       }
       __syncwarp();
       pqn += __popc(bal);
@@ -656,8 +637,7 @@ struct Scanner {
     if (hit) {
       const uint32_t at = pqn + __popc(bal & ((1u << lane) - 1u));
       pq[at] = make_uint2(key, static_cast<uint32_t>(a0 - pbase));
-      const uint32_t lb = A.plan.l2_bits;
-      if (lb) cp_async4(pqw + at, A.l2map + ((key >> (32 - lb)) >> 5));
+
     }
     __syncwarp();
     pqn += __popc(bal);
@@ -970,12 +950,44 @@ __device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
   return r;
 }
 
-__device__ __forceinline__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid,
-                                           uint32_t len) {
+// Exact compare of pattern pid against text[a, a + len) in global memory:
+// 16 pattern bytes at a time against two aligned 16-byte text loads
+// (independent, one round trip per piece) realigned with funnel shifts.
+__device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, uint32_t b) {
+  return __funnelshift_r(lo, hi, b);
+}
+__device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len) {
   const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
-  const uint8_t* t = A.text + a;
-  for (uint32_t i = 0; i < len; ++i)
-    if (__ldg(t + i) != __ldg(p + i)) return false;
+  if (a + len + 32 > A.n) {  // near the end of the text: bytewise (no over-read)
+    const uint8_t* t = A.text + a;
+    for (uint32_t i = 0; i < len; ++i)
+      if (__ldg(t + i) != __ldg(p + i)) return false;
+    return true;
+  }
+  for (uint32_t i = 0; i < len; i += 16) {
+    const unsigned long long x = a + i;
+    const uint4* c = reinterpret_cast<const uint4*>(A.text + (x & ~15ull));
+    const uint4 t0 = __ldg(c), t1 = __ldg(c + 1);
+    const uint4 pv = __ldg(reinterpret_cast<const uint4*>(p + i));
+    const uint32_t sh = static_cast<uint32_t>(x & 15), b = (sh & 3u) * 8u;
+    uint32_t w0, w1, w2, w3, w4;
+    switch (sh >> 2) {
+      case 0: w0 = t0.x; w1 = t0.y; w2 = t0.z; w3 = t0.w; w4 = t1.x; break;
+      case 1: w0 = t0.y; w1 = t0.z; w2 = t0.w; w3 = t1.x; w4 = t1.y; break;
+      case 2: w0 = t0.z; w1 = t0.w; w2 = t1.x; w3 = t1.y; w4 = t1.z; break;
+      default: w0 = t0.w; w1 = t1.x; w2 = t1.y; w3 = t1.z; w4 = t1.w; break;
+    }
+    const uint32_t rem = len - i;  // bytes of this piece that count
+    const uint32_t d0 = fsr(w0, w1, b) ^ pv.x, d1 = fsr(w1, w2, b) ^ pv.y;
+    const uint32_t d2 = fsr(w2, w3, b) ^ pv.z, d3 = fsr(w3, w4, b) ^ pv.w;
+    auto keep = [&](uint32_t word) -> uint32_t {
+      const uint32_t lo = 4u * word;
+      if (rem >= lo + 4) return 0xffffffffu;
+      if (rem <= lo) return 0u;
+      return (1u << (8 * (rem - lo))) - 1u;
+    };
+    if ((d0 & keep(0)) | (d1 & keep(1)) | (d2 & keep(2)) | (d3 & keep(3))) return false;
+  }
   return true;
 }
 
@@ -997,6 +1009,59 @@ __device__ uint32_t window_probe(const ScanArgs& A, unsigned long long a0, uint3
     ++c;
   }
   return c;
+}
+
+// Screen + verify a probe queue (shared by both kernels).  Keys are
+// screened 4 per lane (independent L2 loads, one round trip per 128); the
+// survivors — true matches and ~0.5% strays — are compacted in queue order
+// into `live` (reusing the queue's own storage) so each bucket-walk round
+// serves up to 32 of them.  Output is ordered: queue order = text order.
+__device__ void flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned long long pbase,
+                            uint64_t* out, uint32_t& fill, int lane) {
+  __syncwarp();
+  const uint32_t lb = A.plan.l2_bits;
+  uint32_t nlive = 0;
+  for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
+    const uint32_t i0 = b0 + 4 * lane;
+    uint2 e[4];
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
+      w[j] = ~0u;
+      if (lb && e[j].y != 0xffffffffu) w[j] = __ldg(A.l2map + (screen_bit(e[j].x, lb) >> 5));
+    }
+    uint32_t live = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (e[j].y != 0xffffffffu && (!lb || ((w[j] >> (screen_bit(e[j].x, lb) & 31u)) & 1u))) live |= 1u << j;
+    const uint32_t cnt = __popc(live);
+    const uint32_t excl = warp_excl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
+    __syncwarp();
+    // compact in place: live entries of this block land at nlive + rank (<= i0)
+    uint32_t r = nlive + excl;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (live & (1u << j)) pq[r++] = e[j];
+    __syncwarp();
+    nlive += total;
+  }
+  for (uint32_t i0 = 0; i0 < nlive; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    uint2 e = make_uint2(0u, 0xffffffffu);
+    uint32_t c = 0;
+    if (i < nlive) {
+      e = pq[i];
+      c = window_probe(A, pbase + e.y, e.x, nullptr, 0);
+    }
+    if (!__any_sync(kFull, c != 0)) continue;
+    const uint32_t excl = warp_excl_scan(c, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + c, 31);
+    if (c) window_probe(A, pbase + e.y, e.x, out, fill + excl);
+    fill += total;
+  }
+  __syncwarp();
 }
 
 struct DirectIter {
@@ -1080,7 +1145,7 @@ struct DirectScanner {
       const uint32_t bytes = 16u * d.lim;
       fence_proxy_async();
       mbar_arrive_expect_tx(bars + j, bytes);
-      tma_load_1d(slots + j * kDirectStep, A.text + 16 * d.t, bytes, bars + j);
+      tma_load_1d_stream(slots + j * kDirectStep, A.text + 16 * d.t, bytes, bars + j, policy_evict_first());
     }
   }
 
@@ -1095,37 +1160,8 @@ struct DirectScanner {
   }
 
   __device__ void flush() {
-    __syncwarp();
-    const uint32_t lb = A.plan.l2_bits;
-    for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
-      const uint32_t i0 = b0 + 4 * lane;
-      uint2 e[4];
-      uint32_t w[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        e[j] = i0 + j < pqn ? pq[i0 + j] : make_uint2(0u, 0xffffffffu);
-        w[j] = ~0u;
-        if (lb && e[j].y != 0xffffffffu) w[j] = __ldg(A.l2map + ((e[j].x >> (32 - lb)) >> 5));
-      }
-      uint32_t cnt[4], c = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        cnt[j] = 0;
-        const bool live = e[j].y != 0xffffffffu && (!lb || ((w[j] >> ((e[j].x >> (32 - lb)) & 31u)) & 1u));
-        if (live) cnt[j] = window_probe(A, pbase + e[j].y, e[j].x, nullptr, 0);
-        c += cnt[j];
-      }
-      if (!__any_sync(kFull, c != 0)) continue;
-      const uint32_t excl = warp_excl_scan(c, lane);
-      const uint32_t total = __shfl_sync(kFull, excl + c, 31);
-      uint32_t at = fill + excl;
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (cnt[j]) at += window_probe(A, pbase + e[j].y, e[j].x, out, at);
-      fill += total;
-    }
+    if (!(A.plan.diag & 16)) flush_queue(A, pq, pqn, pbase, out, fill, lane);
     pqn = 0;
-    __syncwarp();
   }
 
   // hit lanes queue {window key, 16 * sample - pbase}
@@ -1142,7 +1178,13 @@ struct DirectScanner {
   __device__ __forceinline__ void half(const uint4& v, bool valid, uint32_t pos) {
     const uint32_t h = hash_gram_words(v.x, v.y, v.z, v.w);
     const bool hit = valid && admits(h);
-    const uint32_t key = key_words(v.x & km[0], v.y & km[1], v.z & km[2], v.w & km[3]);
+    if (!__any_sync(kFull, hit)) return;
+    if (A.plan.diag & 8) {  // diagnostics: count only
+      cands32 += hit ? 1u : 0u;
+      return;
+    }
+    const uint32_t key =
+        A.plan.key_gram ? h : key_words(v.x & km[0], v.y & km[1], v.z & km[2], v.w & km[3]);
     push(hit, key, pos);
   }
 
