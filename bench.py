@@ -8,6 +8,11 @@ text through the fused sm_100a kernel up to the sorted (offset, pattern)
 match array in HBM.  The text (1 GiB) is larger than L2 (126 MB), so no L2
 flush is needed between steps.
 
+N > 1 (torchrun, one rank per GPU): weak scaling over a text of N copies of
+the workload text.  Rank g owns start offsets [g*n, (g+1)*n) and searches its
+1 GiB plus maxlen-1 halo bytes (shard.py); the only exchange is the gather
+of the per-rank sorted match lists, which the e2e leg includes.
+
 Arms:
   default            our library; `value` = device-resident GB/s (CUDA events,
                      max over ranks), `e2e` = the same metric through
@@ -50,29 +55,61 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region (NVML,
+    every ~2 ms; nvidia-smi when NVML is unavailable)."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [reason flags])
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            pr = torch.cuda.get_device_properties(gpu)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            try:
+                h = N.nvmlDeviceGetHandleByPciBusId_v2(bus.encode())
+            except Exception:
+                h = N.nvmlDeviceGetHandleByIndex(gpu)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            self._nvml = (N, h, bits, mx)
+        except Exception:
+            self._nvml = None
 
-    def _run(self):
+    def _sample_nvml(self):
+        N, h, bits, mx = self._nvml
+        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        return (float(sm), float(mx), [bool(r & b) for b in bits])
+
+    def _sample_smi(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        f = [x.strip() for x in out.split(",")]
+        if len(f) < 6:
+            return None
+        return (float(f[0]), float(f[1]), [x.lower() == "active" for x in f[2:6]])
+
+    def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                f = [x.strip() for x in out.split(",")]
-                if len(f) >= 6:
-                    self.samples.append(f)
+                x = self._sample_nvml() if self._nvml else self._sample_smi()
+                if x:
+                    self.samples.append(x)
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.002 if self._nvml else 0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -86,12 +123,10 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+        sm = sorted(s[0] for s in self.samples)
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[2][i]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
 def cpu_reference(workload, budget_s=12.0, threads=None):
@@ -141,10 +176,10 @@ def main():
         w = workloads.generate(args.config, args.scale)
         vals = []
         for _ in range(max(args.warmup, 0)):
-            cpu_reference(w, budget_s=3.0)
+            cpu_reference(w, budget_s=1.0)
         info = None
         for _ in range(max(args.steps, 1)):
-            gbs, cores, sample, kind = cpu_reference(w, budget_s=6.0)
+            gbs, cores, sample, kind = cpu_reference(w, budget_s=4.0)
             vals.append(gbs)
             info = (cores, sample, kind)
         v = sorted(vals)[len(vals) // 2]
@@ -172,12 +207,16 @@ def main():
         if world > 1:
             dist.barrier()
 
+    from paper_1405_5483_b200 import shard
     w = workloads.generate(args.config, args.scale)
     n = int(w.text.size)
+    maxlen = max(len(p) for p in w.patterns)
+    # this rank's read span of the N-copy text: its own copy + the next copy's first maxlen-1 bytes
+    span = w.text if rank == world - 1 else np.concatenate([w.text, w.text[:maxlen - 1]])
     eng = mag.Engine(w.patterns, device=local)
     plan = eng.plan()
-    d_text = torch.from_numpy(w.text).to(f"cuda:{local}")
-    prep = eng.prepare_device(d_text.data_ptr(), n, keep=d_text)
+    d_text = torch.from_numpy(span).to(f"cuda:{local}")
+    prep = eng.prepare_device(d_text.data_ptr(), span.size, keep=d_text)
     stream = torch.cuda.Stream()
 
     # correctness anchor for this very text: one full materialised search
@@ -220,8 +259,8 @@ def main():
     value = world * n / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through mag_search (pinned host text in, host matches out)
-    pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-    pinned.numpy()[:] = w.text
+    pinned = torch.empty(span.size, dtype=torch.uint8, pin_memory=True)
+    pinned.numpy()[:] = span
     host = pinned.numpy()
     m = eng.search(host)  # warm the host-text workspace
     m.close()
@@ -229,12 +268,18 @@ def main():
     barrier()
     e2e_t = []
     d2h = 0
+    total_matches = None
     for _ in range(max(args.e2e_steps, 1)):
+        barrier()
         t0 = time.perf_counter()
         m = eng.search(host)
-        cnt = len(m)
+        offs, pids = m.arrays()
+        offs, pids = shard.clip(offs, pids, 0, n)
+        got = shard.gather(offs + np.uint64(rank * n), pids, world, rank)
         e2e_t.append(time.perf_counter() - t0)
-        d2h = cnt * 8 + 32
+        d2h = len(m) * 12 + 32
+        if got is not None:
+            total_matches = int(got[0].size)
         m.close()
     e2e_s = sorted(e2e_t)[len(e2e_t) // 2]
     te = torch.tensor([e2e_s], device=f"cuda:{local}")
@@ -267,20 +312,20 @@ def main():
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": w.name, "n": n, "r": len(w.patterns), "m": w.meta["m"],
-                   "parallelism": f"text replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"text shards x{world} (N copies, halo maxlen-1)" if world > 1 else "single GPU",
                    "l2": "input (1 GiB) larger than L2; no flush needed" if n > (126 << 20)
                    else "input smaller than L2 (not flushed)",
                    "plan": {k: plan[k] for k in ("variant", "gram_mode", "q", "k", "m_prime", "table_bits",
                                                  "entry_bits", "verify_all", "prefilter_bits", "tile_bytes",
                                                  "warps", "stages", "smem_bytes")},
-                   "matches": n_matches, "filter_reads": metrics.filter_reads,
+                   "matches": n_matches, "job_matches": total_matches, "filter_reads": metrics.filter_reads,
                    "candidates": metrics.candidates, "checked_vs_reference_ac": checked},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": n},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": n, "d2h_bytes_per_step": d2h,
-                "api": "mag_search (pinned host text)"},
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(span.size), "d2h_bytes_per_step": d2h,
+                "api": "mag_search (pinned host text) + clip + rank-ordered gather"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
     }

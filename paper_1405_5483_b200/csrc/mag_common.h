@@ -177,7 +177,7 @@ constexpr int kDirectDepth = 4;
 constexpr int kDirectStep = 64;  // samples per step (1 KiB of text)
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
-         size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * 8 + 64;
+         size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * (16 + 8) + 64;
 }
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,

@@ -133,8 +133,8 @@ __device__ __forceinline__ bool bloom_admits(const unsigned long long* tab, cons
 }
 
 __device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len);
-__device__ void flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned long long pbase,
-                            uint64_t* out, uint32_t& fill, int lane);
+__device__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned long long pbase,
+                                uint64_t* out, uint32_t fill, int lane, bool screened = false);
 
 // Gram formation modes for the kernel template.
 enum KGram : int { kKExact = 0, kKHashed = 1, kKCodes = 2 };
@@ -483,7 +483,7 @@ struct Scanner {
   // trip covers 128 windows.  Survivors walk their bucket.
   __device__ void flush_pq() {
     cp_async_wait_all();
-    if (!(A.plan.diag & 2)) flush_queue(A, pq, pqn, pbase, out, fill, lane);
+    if (!(A.plan.diag & 2)) fill = flush_queue(A, pq, pqn, pbase, out, fill, lane);
     pqn = 0;
   }
 
@@ -1016,12 +1016,13 @@ __device__ uint32_t window_probe(const ScanArgs& A, unsigned long long a0, uint3
 // survivors — true matches and ~0.5% strays — are compacted in queue order
 // into `live` (reusing the queue's own storage) so each bucket-walk round
 // serves up to 32 of them.  Output is ordered: queue order = text order.
-__device__ void flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned long long pbase,
-                            uint64_t* out, uint32_t& fill, int lane) {
+__device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn,
+                                             unsigned long long pbase, uint64_t* out, uint32_t fill, int lane,
+                                             bool screened) {
   __syncwarp();
   const uint32_t lb = A.plan.l2_bits;
-  uint32_t nlive = 0;
-  for (uint32_t b0 = 0; b0 < pqn; b0 += 4 * 32) {
+  uint32_t nlive = screened ? pqn : 0;
+  for (uint32_t b0 = 0; !screened && b0 < pqn; b0 += 4 * 32) {
     const uint32_t i0 = b0 + 4 * lane;
     uint2 e[4];
     uint32_t w[4];
@@ -1062,13 +1063,8 @@ __device__ void flush_queue(const ScanArgs& A, uint2* pq, uint32_t pqn, unsigned
     fill += total;
   }
   __syncwarp();
+  return fill;
 }
-
-struct DirectIter {
-  unsigned long long slice, t;  // owning slice, first sample of the step
-  uint32_t lim;                 // valid samples in the step (<= 64)
-  uint32_t flags;               // 1 first step of its slice, 2 last, 4 valid
-};
 
 // Multi-probe membership on a 64-entry block given as two words.
 template <int H>
@@ -1083,69 +1079,82 @@ __device__ __forceinline__ bool bloom_admits_w(uint32_t lo, uint32_t hi, uint32_
   return !(m & 1u);
 }
 
+// Step descriptor, written by lane 0 when the step's TMA is issued and read
+// by the whole warp when the step is consumed: x first sample, y slice,
+// z valid samples | flags << 8 (1 first step of its slice, 2 last, 4 valid).
+struct __align__(16) DirectDesc {
+  uint32_t t, slice, lim_flags, pad;
+};
+
 template <int H>
 struct DirectScanner {
   const ScanArgs& A;
   const int lane;
   const void* table;
   uint2* pq;
-  uint4* slots;    // [kDirectDepth][kDirectStep] staged samples
-  uint64_t* bars;  // [kDirectDepth]
+  uint4* slots;       // [kDirectDepth][kDirectStep] staged samples
+  uint64_t* bars;     // [kDirectDepth]
+  DirectDesc* desc;   // [kDirectDepth]
   uint32_t pqn, fill, cands32;
-  unsigned long long pbase;
+  uint32_t pbase_t;   // first sample of the current slice
   uint64_t* out;
-  uint32_t km[4];  // window-key word masks
-  // slice stream (warp-uniform)
-  unsigned long long s_slice, s_t;
-  uint32_t s_left;  // samples left in the slice
-  bool s_done, s_first;
+  uint32_t pend_w[2], pend_b[2], pend_k[2], pend_pos;  // screen loads in flight
+  // producer cursor (warp-uniform)
+  uint32_t p_t, p_left;
+  bool p_done;
 
-  __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint4* sl, uint64_t* b, int l)
-      : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), pqn(0), fill(0), cands32(0), pbase(0),
-        out(nullptr) {
-    for (int i = 0; i < 4; ++i) km[i] = key_word_mask(A.plan.wkey_len, i);
-    s_slice = s_t = 0;
-    s_left = 0;
-    s_done = false;
-    s_first = false;
+  __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint4* sl, uint64_t* b, DirectDesc* dsc,
+                           int l)
+      : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
+        pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false) {
+    pend_w[0] = pend_w[1] = pend_b[0] = pend_b[1] = pend_k[0] = pend_k[1] = pend_pos = 0;
   }
 
-  __device__ __forceinline__ void next(DirectIter& d) {
-    while (!s_done && s_left == 0) {
+  // Claim the next step and stage it into ring slot j (TMA bulk copy,
+  // completion on bars[j]); an invalid descriptor marks the end.
+  __device__ __forceinline__ void produce(int j) {
+    uint32_t slice = 0;
+    bool first = false;
+    while (!p_done && p_left == 0) {
       unsigned long long x = 0;
       if (lane == 0) x = atomicAdd(A.ticket, 1ull);
       x = __shfl_sync(kFull, x, 0) + A.slice_begin;
       if (x >= A.slice_end) {
-        s_done = true;
+        p_done = true;
         break;
       }
-      s_slice = x;
-      s_t = x * A.slice_samples;
-      const unsigned long long end = s_t + A.slice_samples < A.samples ? s_t + A.slice_samples : A.samples;
-      s_left = end > s_t ? static_cast<uint32_t>(end - s_t) : 0u;
-      s_first = true;
-      if (s_left == 0 && lane == 0) A.slice_count[x] = 0;
+      const unsigned long long t0 = x * A.slice_samples;
+      const unsigned long long t1 = t0 + A.slice_samples < A.samples ? t0 + A.slice_samples : A.samples;
+      if (t1 <= t0) {
+        if (lane == 0) A.slice_count[x] = 0;
+        continue;
+      }
+      slice = static_cast<uint32_t>(x);
+      p_t = static_cast<uint32_t>(t0);
+      p_left = static_cast<uint32_t>(t1 - t0);
+      first = true;
     }
-    if (s_done) {
-      d.flags = 0;
-      return;
-    }
-    d.slice = s_slice;
-    d.t = s_t;
-    d.lim = s_left < 64u ? s_left : 64u;
-    d.flags = 4u | (s_first ? 1u : 0u) | (s_left <= 64u ? 2u : 0u);
-    s_first = false;
-    s_t += d.lim;
-    s_left -= d.lim;
-  }
-
-  // Stage step d into ring slot j (TMA bulk copy, completion on bar[j]).
-  __device__ __forceinline__ void issue(const DirectIter& d, int j) {
     if (lane == 0) {
-      const uint32_t bytes = 16u * d.lim;
-      fence_proxy_async();
-      mbar_arrive_expect_tx(bars + j, bytes);
-      tma_load_1d_stream(slots + j * kDirectStep, A.text + 16 * d.t, bytes, bars + j, policy_evict_first());
+      DirectDesc d;
+      if (p_done) {
+        d.t = d.slice = d.lim_flags = d.pad = 0;
+      } else {
+        const uint32_t lim = p_left < 64u ? p_left : 64u;
+        d.t = p_t;
+        d.slice = first ? slice : desc[(j + kDirectDepth - 1) & (kDirectDepth - 1)].slice;
+        d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= 64u ? 2u : 0u)) << 8);
+        d.pad = 0;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(bars + j, 16u * lim);
+        tma_load_1d_stream(slots + j * kDirectStep, A.text + 16ull * p_t, 16u * lim, bars + j,
+                           policy_evict_first());
+      }
+      desc[j] = d;
+    }
+    if (!p_done) {
+      const uint32_t lim = p_left < 64u ? p_left : 64u;
+      p_t += lim;
+      p_left -= lim;
     }
   }
 
@@ -1159,77 +1168,96 @@ struct DirectScanner {
     }
   }
 
-  __device__ void flush() {
-    if (!(A.plan.diag & 16)) flush_queue(A, pq, pqn, pbase, out, fill, lane);
+  __device__ __forceinline__ void flush() {
+    if (!(A.plan.diag & 16))
+      fill = flush_queue(A, pq, pqn, 16ull * pbase_t, out, fill, lane, true);
     pqn = 0;
   }
 
-  // hit lanes queue {window key, 16 * sample - pbase}
+  // survivors queue {window key, 16 * sample - pbase}
   __device__ __forceinline__ void push(bool hit, uint32_t key, uint32_t pos) {
     const unsigned bal = __ballot_sync(kFull, hit);
     if (!bal) return;
-    cands32 += hit ? 1u : 0u;
     if (pqn + __popc(bal) > kProbeCap) flush();
     if (hit) pq[pqn + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key, pos);
     __syncwarp();
     pqn += __popc(bal);
   }
 
-  __device__ __forceinline__ void half(const uint4& v, bool valid, uint32_t pos) {
+  // Filter one sample; a filter hit issues its L2 screen load now and is
+  // resolved one step later (resolve()), so the L2 round trip overlaps the
+  // next step's filtering instead of stalling the warp.
+  __device__ __forceinline__ void half(const uint4& v, bool valid, int i) {
     const uint32_t h = hash_gram_words(v.x, v.y, v.z, v.w);
     const bool hit = valid && admits(h);
-    if (!__any_sync(kFull, hit)) return;
-    if (A.plan.diag & 8) {  // diagnostics: count only
-      cands32 += hit ? 1u : 0u;
-      return;
+    cands32 += hit ? 1u : 0u;
+    pend_w[i] = 0;
+    if (A.plan.diag & 8) return;  // diagnostics: count only
+    uint32_t key = h;
+    if (!A.plan.key_gram) {
+      const uint32_t wl = A.plan.wkey_len;
+      key = key_words(v.x & key_word_mask(wl, 0), v.y & key_word_mask(wl, 1), v.z & key_word_mask(wl, 2),
+                      v.w & key_word_mask(wl, 3));
     }
-    const uint32_t key =
-        A.plan.key_gram ? h : key_words(v.x & km[0], v.y & km[1], v.z & km[2], v.w & km[3]);
-    push(hit, key, pos);
+    pend_k[i] = key;
+    const uint32_t lb = A.plan.l2_bits;
+    if (hit) {
+      if (lb) {
+        const uint32_t sb = screen_bit(key, lb);
+        pend_b[i] = sb & 31u;
+        pend_w[i] = __ldg(A.l2map + (sb >> 5));
+      } else {
+        pend_b[i] = 0;
+        pend_w[i] = 1u;
+      }
+    }
   }
 
-  __device__ __forceinline__ void process(const DirectIter& d, const uint4& a, const uint4& b) {
-    if (d.flags & 1u) {
+  __device__ __forceinline__ void resolve() {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) push((pend_w[i] >> pend_b[i]) & 1u, pend_k[i], pend_pos + 512u * i);
+    pend_w[0] = pend_w[1] = 0;
+  }
+
+  __device__ __forceinline__ void process(const DirectDesc& d, const uint4& a, const uint4& b) {
+    const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
+    if (flags & 1u) {
       fill = 0;
       pqn = 0;
-      pbase = 16 * d.t;
+      pbase_t = d.t;
       out = A.staging + static_cast<size_t>(d.slice) * A.slice_cap;
+    } else {
+      resolve();  // the previous step of this slice
     }
-    const uint32_t pos0 = static_cast<uint32_t>(16 * d.t - pbase) + 16u * lane;
-    half(a, static_cast<uint32_t>(lane) < d.lim, pos0);
-    half(b, static_cast<uint32_t>(lane) + 32 < d.lim, pos0 + 512u);
-    if (d.flags & 2u) {
+    pend_pos = 16u * (d.t - pbase_t) + 16u * lane;
+    half(a, static_cast<uint32_t>(lane) < lim, 0);
+    half(b, static_cast<uint32_t>(lane) + 32 < lim, 1);
+    if (flags & 2u) {
+      resolve();
       if (pqn) flush();
       if (lane == 0) A.slice_count[d.slice] = fill;
     }
   }
 
   __device__ void run() {
-    DirectIter d[kDirectDepth];
-#pragma unroll
-    for (int j = 0; j < kDirectDepth; ++j) {
-      next(d[j]);
-      if (d[j].flags & 4u) issue(d[j], j);
-    }
+#pragma unroll 1
+    for (int j = 0; j < kDirectDepth; ++j) produce(j);
+    __syncwarp();
     uint32_t phase = 0;  // bit j: parity of slot j's next completion
-    bool more = true;
-    while (more) {
-#pragma unroll
-      for (int j = 0; j < kDirectDepth; ++j) {
-        if (!(d[j].flags & 4u)) {
-          more = false;
-          break;
-        }
-        mbar_wait(bars + j, (phase >> j) & 1u);
-        phase ^= 1u << j;
-        const uint4 a = slots[j * kDirectStep + lane];
-        const uint4 b = slots[j * kDirectStep + 32 + lane];
-        const DirectIter cur = d[j];
-        __syncwarp();
-        next(d[j]);
-        if (d[j].flags & 4u) issue(d[j], j);  // refill the slot just read
-        process(cur, a, b);
-      }
+    int j = 0;
+#pragma unroll 1
+    while (true) {
+      const DirectDesc d = desc[j];
+      if (!(d.lim_flags & 0x400u)) break;  // steps are issued in order: first invalid = end
+      mbar_wait(bars + j, (phase >> j) & 1u);
+      phase ^= 1u << j;
+      const uint4 a = slots[j * kDirectStep + lane];
+      const uint4 b = slots[j * kDirectStep + 32 + lane];
+      __syncwarp();
+      produce(j);  // refill the slot just read
+      __syncwarp();
+      process(d, a, b);
+      j = (j + 1) & (kDirectDepth - 1);
     }
     unsigned long long c = cands32;
 #pragma unroll
@@ -1254,13 +1282,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_direct_kernel(const __g
   p += align16(size_t(nw) * kProbeCap * 8);
   uint4* slots = reinterpret_cast<uint4*>(p) + static_cast<size_t>(warp) * kDirectDepth * kDirectStep;
   p += size_t(nw) * kDirectDepth * kDirectStep * 16;
+  DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * kDirectDepth;
+  p += size_t(nw) * kDirectDepth * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kDirectDepth;
   if ((threadIdx.x & 31) == 0) {
     for (int j = 0; j < kDirectDepth; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  DirectScanner<H> ds(A, smem, pq, slots, bars, threadIdx.x & 31);
+  DirectScanner<H> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
   ds.run();
 }
 
@@ -1299,8 +1329,12 @@ cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
 __global__ void __launch_bounds__(1024) mag_compact_kernel(const __grid_constant__ ScanArgs A,
                                                             uint64_t* __restrict__ out,
                                                             uint64_t out_cap) {
+  // Block b owns slices [s0, s1): its base is the sum of every earlier
+  // slice's count (parallel reduction), then the owned slices are scanned
+  // 1024 at a time in shared memory and each warp copies whole slices.
   __shared__ unsigned long long red[32];
-  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_pre[1024];
+  __shared__ uint32_t s_cnt[1024];
   const uint64_t ns = A.num_slices;
   const uint64_t per = (ns + gridDim.x - 1) / gridDim.x;
   uint64_t s0 = blockIdx.x * per;
@@ -1308,38 +1342,63 @@ __global__ void __launch_bounds__(1024) mag_compact_kernel(const __grid_constant
   uint64_t s1 = s0 + per;
   if (s1 > ns) s1 = ns;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  unsigned long long acc = 0, mx = 0;
+  unsigned long long acc = 0;
   for (uint64_t i = tid; i < s0; i += blockDim.x) acc += A.slice_count[i];
-  for (uint64_t i = s0 + tid; i < s1; i += blockDim.x) {
-    const unsigned long long c = A.slice_count[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane == 0) red[wid] = acc;
+  __syncthreads();
+  unsigned long long base = 0;
+  for (int w = 0; w < nw; ++w) base += red[w];
+  __syncthreads();
+  uint32_t mx = 0;
+  for (uint64_t c0 = s0; c0 < s1; c0 += blockDim.x) {
+    const uint64_t s = c0 + tid;
+    const uint32_t c = s < s1 ? A.slice_count[s] : 0u;
     mx = c > mx ? c : mx;
+    // block-wide exclusive scan of c
+    unsigned long long v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) red[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+      unsigned long long t = lane < nw ? red[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, t, o);
+        if (lane >= o) t += y;
+      }
+      red[lane] = t;  // inclusive warp totals
+    }
+    __syncthreads();
+    const unsigned long long wbase = wid ? red[wid - 1] : 0;
+    s_pre[tid] = base + wbase + v - c;
+    s_cnt[tid] = c;
+    const unsigned long long total = red[nw - 1];
+    __syncthreads();
+    const int len = static_cast<int>(s1 - c0 < blockDim.x ? s1 - c0 : blockDim.x);
+    for (int j = wid; j < len; j += nw) {
+      const uint32_t cj = s_cnt[j];
+      if (!cj) continue;
+      const uint32_t cc = cj < A.slice_cap ? cj : A.slice_cap;
+      const uint64_t* srcp = A.staging + (c0 + j) * A.slice_cap;
+      const unsigned long long b = s_pre[j];
+      for (uint32_t i = lane; i < cc; i += 32)
+        if (b + i < out_cap) out[b + i] = srcp[i];
+    }
+    base += total;
+    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
-    acc += __shfl_xor_sync(kFull, acc, o);
-    const unsigned long long y = __shfl_xor_sync(kFull, mx, o);
+    const uint32_t y = __shfl_xor_sync(kFull, mx, o);
     mx = y > mx ? y : mx;
   }
-  if (lane == 0) red[wid] = acc;
-  if (lane == 0 && mx) atomicMax(A.counters + 3, mx);
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long b = 0;
-    for (int w = 0; w < nw; ++w) b += red[w];
-    s_base = b;
-  }
-  __syncthreads();
-  unsigned long long base = s_base;
-  for (uint64_t s = s0; s < s1; ++s) {
-    const unsigned long long c = A.slice_count[s];
-    if (c) {
-      const unsigned long long cc = c < A.slice_cap ? c : A.slice_cap;
-      const uint64_t* srcp = A.staging + s * A.slice_cap;
-      for (unsigned long long i = tid; i < cc; i += blockDim.x)
-        if (base + i < out_cap) out[base + i] = srcp[i];
-    }
-    base += c;
-  }
+  if (lane == 0 && mx) atomicMax(A.counters + 3, static_cast<unsigned long long>(mx));
   if (blockIdx.x == gridDim.x - 1 && tid == 0) A.counters[2] = base;
 }
 

@@ -213,3 +213,63 @@ def test_baseline_configs_reduced(mag, ref, cfg, scale):
     offs, pids = m.arrays()
     assert np.array_equal(offs, want[0]) and np.array_equal(pids, want[1]), (cfg, e.plan())
     assert m.metrics().filter_reads == (w.text.size // e.info().q) // e.info().k or e.plan()["verify_all"]
+
+
+def _golden():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+
+
+def _unpack(g, key):
+    b, l = g[f"{key}_pat"], g[f"{key}_len"]
+    out, o = [], 0
+    for n in l.tolist():
+        out.append(b[o:o + n].tobytes())
+        o += n
+    return out
+
+
+def test_golden_fixtures(mag):
+    """CUDA path vs the reference's own outputs (tests/golden, generated by
+    the compiled reference; no /root/reference needed on the GPU box)."""
+    g = _golden()
+    keys = [f"spec_{i}" for i in range(6)] + [f"inst_{i}" for i in range(int(g["inst_count"][0]))]
+    for key in keys:
+        text, pats = g[f"{key}_text"], _unpack(g, key)
+        want = as_pairs(g[f"{key}_off"], g[f"{key}_pid"])
+        for variant in ("mag", "smag", "shiftor_og"):
+            e = mag.Engine(pats, variant=variant)
+            assert gpu_pairs(e, text)[0] == want, (key, variant, e.plan())
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_golden_configs(mag, cfg):
+    from paper_1405_5483_b200 import workloads
+    g = _golden()
+    w = workloads.generate(cfg, float(g[f"cfg_{cfg}_scale"][0]))
+    offs, pids = mag.Engine(w.patterns).search(w.text).arrays()
+    assert np.array_equal(offs, g[f"cfg_{cfg}_off"]) and np.array_equal(pids, g[f"cfg_{cfg}_pid"])
+
+
+def test_sharded_spans(mag, ref):
+    """shard.py over device-resident text: every rank's span searched in
+    place, clipped and concatenated in rank order == the whole-text result."""
+    import torch
+    from paper_1405_5483_b200 import shard
+    rng = np.random.default_rng(12)
+    text, pats = rand_instance(rng, sig=4, n=1 << 20, r=300, m=24, base=65)
+    want = ref.ac(text, pats)
+    e = mag.Engine(pats)
+    d = torch.from_numpy(text).cuda()
+    run = shard.engine_span_search(e, d.data_ptr(), keep=d)
+    maxlen = max(len(p) for p in pats)
+    for world in (2, 3, 8):
+        b = shard.ownership(text.size, world)
+        parts = []
+        for g in range(world):
+            lo, hi = shard.read_span(text.size, b, g, maxlen)
+            o, p = run(lo, hi) if hi > lo else (np.zeros(0, np.uint64), np.zeros(0, np.uint32))
+            parts.append(shard.clip(o, p, lo, b[g + 1]))
+        offs = np.concatenate([x[0] for x in parts])
+        pids = np.concatenate([x[1] for x in parts])
+        assert np.array_equal(offs, want[0]) and np.array_equal(pids, want[1]), world

@@ -37,10 +37,14 @@ for _ in range(2):  # warm-up: lazy module load, workspace allocation
     e.search_prepared_async(p, s.cuda_stream).close()
 torch.cuda.synchronize()
 mag.scan_timer(True)
+ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ev0.record(s)
 for _ in range(a.iters):
     e.search_prepared_async(p, s.cuda_stream).close()
+ev1.record(s)
 torch.cuda.synchronize()
+step_ms = ev0.elapsed_time(ev1) / a.iters
 ms, n = mag.scan_timer_read()
 m = e.search_prepared(p)
 print(f"{w.name} plan={e.plan()} matches={len(m)} metrics={m.metrics()} kernel_ms={ms / max(n, 1):.3f} "
-      f"GB/s={w.text.size / (ms / max(n, 1)) / 1e6:.1f}")
+      f"GB/s={w.text.size / (ms / max(n, 1)) / 1e6:.1f} step_ms={step_ms:.3f} step_GB/s={w.text.size / step_ms / 1e6:.1f}")
