@@ -56,7 +56,11 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // Per-search device scratch, pooled per engine.  `done` orders reuse on the
 // device (a later search waits for it with cudaStreamWaitEvent).
 struct Workspace {
-  unsigned long long* ctrl = nullptr;  // counters[8] | tickets[kMaxLaunch]
+  // two halves of counters[8] | tickets[kMaxLaunch]: a search uses half
+  // `parity` and its compaction kernel zeroes the other half for the next
+  // search on this workspace (no memset launch per search)
+  unsigned long long* ctrl = nullptr;
+  uint32_t parity = 0;
   uint32_t* counts = nullptr;          // per-slice match counts
   size_t counts_cap = 0;
   uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
@@ -221,6 +225,7 @@ void release(const mag_engine* e, std::unique_ptr<Workspace> w) {
 }
 
 constexpr size_t kCounters = 8;
+constexpr size_t kCtrlWords = kCounters + kMaxLaunch;
 
 struct SearchGeometry {
   uint64_t samples, num_slices, slice_cap;
@@ -251,7 +256,11 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
 mag_status ensure_ws(Workspace* w, const SearchGeometry& g) {
   if (!w->done) MAG_CUDA(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
   if (!w->h_ctr) MAG_CUDA(cudaMallocHost(&w->h_ctr, kCounters * sizeof(unsigned long long)));
-  if (!w->ctrl) MAG_CUDA(cudaMalloc(&w->ctrl, (kCounters + kMaxLaunch) * sizeof(unsigned long long)));
+  if (!w->ctrl) {
+    MAG_CUDA(cudaMalloc(&w->ctrl, 2 * kCtrlWords * sizeof(unsigned long long)));
+    MAG_CUDA(cudaMemset(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long)));
+    w->parity = 0;
+  }
   if (w->counts_cap < std::max<uint64_t>(1, g.num_slices)) {
     if (w->counts) MAG_CUDA(cudaFree(w->counts));
     w->counts = nullptr;
@@ -288,8 +297,9 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   if (s != MAG_OK) return s;
   w->num_slices = g.num_slices;
   w->slice_cap = g.slice_cap;
-  MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, (kCounters + kMaxLaunch) * sizeof(unsigned long long), st));
-  unsigned long long* counters = w->ctrl;
+  unsigned long long* counters = w->ctrl + w->parity * kCtrlWords;
+  unsigned long long* next_ctrl = w->ctrl + (w->parity ^ 1u) * kCtrlWords;
+  w->parity ^= 1u;
   if (g.num_slices) {
     ScanArgs a{};
     a.plan = P.sp;
@@ -325,14 +335,19 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
       if (r.end <= r.begin) continue;
       a.slice_begin = r.begin;
       a.slice_end = r.end;
-      a.ticket = counters + kCounters + (li++ % kMaxLaunch);
+      if (li >= kMaxLaunch) return fail(MAG_ERR_INTERNAL, "too many scan launches for one search");
+      a.ticket = counters + kCounters + li++;
       const uint64_t ctas = (r.end - r.begin + P.nwarps - 1) / P.nwarps;
       const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
       MAG_CUDA(timed_launch(a, st, grid));
     }
     const int cgrid = static_cast<int>(std::min<uint64_t>(
         std::max<uint64_t>(1, g.num_slices / 8), static_cast<uint64_t>(e->sm_count)));
+    a.reset = next_ctrl;
+    a.reset_words = static_cast<uint32_t>(kCtrlWords);
     MAG_CUDA(launch_compact(a, w->out, w->out_cap, st, cgrid));
+  } else {
+    MAG_CUDA(cudaMemsetAsync(next_ctrl, 0, kCtrlWords * sizeof(unsigned long long), st));
   }
   MAG_CUDA(cudaMemcpyAsync(w->h_ctr, counters, kCounters * sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, st));

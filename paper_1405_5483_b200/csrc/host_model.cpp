@@ -244,7 +244,8 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostWindow = 60, kCostScreen = 25, kCostProbe = 80, kCostVerifyAll = 45, kCostCompare = 40,
                  kCostChunk = 4800,  // per staged chunk (loader + bookkeeping), thread-instr
                  kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
-                 kCostPf = 15;       // shared-memory prefilter test
+                 kCostPf = 15,       // shared-memory prefilter test
+                 kCostDirectHit = 6;  // direct kernel: a filter hit issues one L2 screen load
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -544,8 +545,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / bits);
         const double p = exact + (1.0 - exact) * std::pow(fill, static_cast<double>(H));
         const double cpb = p / q;
+        // a filter hit only issues its L2 screen load (resolved a step later);
+        // ~1/128 of them, plus the true starts, reach a bucket walk
         const double cost = (kCostSample + H * kCostProbeBit) / q +
-                            cpb * (kCostCand + kCostScreen + 0.01 * kCostProbe + hits * kCostCompare);
+                            cpb * (kCostDirectHit + 0.008 * (kCostCand + kCostProbe + hits * kCostCompare));
         if (cost < best.cost * 0.999) {
           best.cost = cost;
           best.q = q;

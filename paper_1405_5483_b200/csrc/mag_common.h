@@ -174,7 +174,7 @@ struct SmemLayout {
 // Direct (q = 16) kernel: resident table, per-warp probe queue, and a ring
 // of kDirectDepth 1 KiB step buffers (+ mbarriers) per warp.
 constexpr int kDirectDepth = 4;
-constexpr int kDirectStep = 64;  // samples per step (1 KiB of text)
+constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lane
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
          size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * (16 + 8) + 64;

@@ -897,6 +897,8 @@ struct Scanner {
 
 template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK, bool A4>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
+  // let the dependent gather grid launch early (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
   Smem S;
@@ -1098,7 +1100,9 @@ struct DirectScanner {
   uint32_t pqn, fill, cands32;
   uint32_t pbase_t;   // first sample of the current slice
   uint64_t* out;
-  uint32_t pend_w[2], pend_b[2], pend_k[2], pend_pos;  // screen loads in flight
+  static constexpr uint32_t kStep = kDirectStep;
+  static constexpr int kPer = kDirectStep / 32;  // samples per lane per step
+  uint32_t pend_w[kPer], pend_b[kPer], pend_k[kPer], pend_pos;  // screen loads in flight
   // producer cursor (warp-uniform)
   uint32_t p_t, p_left;
   bool p_done;
@@ -1107,7 +1111,8 @@ struct DirectScanner {
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
         pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false) {
-    pend_w[0] = pend_w[1] = pend_b[0] = pend_b[1] = pend_k[0] = pend_k[1] = pend_pos = 0;
+    for (int i = 0; i < kPer; ++i) pend_w[i] = pend_b[i] = pend_k[i] = 0;
+    pend_pos = 0;
   }
 
   // Claim the next step and stage it into ring slot j (TMA bulk copy,
@@ -1139,12 +1144,11 @@ struct DirectScanner {
       if (p_done) {
         d.t = d.slice = d.lim_flags = d.pad = 0;
       } else {
-        const uint32_t lim = p_left < 64u ? p_left : 64u;
+        const uint32_t lim = p_left < kStep ? p_left : kStep;
         d.t = p_t;
-        d.slice = first ? slice : desc[(j + kDirectDepth - 1) & (kDirectDepth - 1)].slice;
-        d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= 64u ? 2u : 0u)) << 8);
+        d.slice = first ? slice : desc[j == 0 ? kDirectDepth - 1 : j - 1].slice;
+        d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= kStep ? 2u : 0u)) << 8);
         d.pad = 0;
-        fence_proxy_async();
         mbar_arrive_expect_tx(bars + j, 16u * lim);
         tma_load_1d_stream(slots + j * kDirectStep, A.text + 16ull * p_t, 16u * lim, bars + j,
                            policy_evict_first());
@@ -1152,7 +1156,7 @@ struct DirectScanner {
       desc[j] = d;
     }
     if (!p_done) {
-      const uint32_t lim = p_left < 64u ? p_left : 64u;
+      const uint32_t lim = p_left < kStep ? p_left : kStep;
       p_t += lim;
       p_left -= lim;
     }
@@ -1184,42 +1188,44 @@ struct DirectScanner {
     pqn += __popc(bal);
   }
 
-  // Filter one sample; a filter hit issues its L2 screen load now and is
-  // resolved one step later (resolve()), so the L2 round trip overlaps the
-  // next step's filtering instead of stalling the warp.
-  __device__ __forceinline__ void half(const uint4& v, bool valid, int i) {
-    const uint32_t h = hash_gram_words(v.x, v.y, v.z, v.w);
-    const bool hit = valid && admits(h);
-    cands32 += hit ? 1u : 0u;
-    pend_w[i] = 0;
-    if (A.plan.diag & 8) return;  // diagnostics: count only
-    uint32_t key = h;
-    if (!A.plan.key_gram) {
-      const uint32_t wl = A.plan.wkey_len;
-      key = key_words(v.x & key_word_mask(wl, 0), v.y & key_word_mask(wl, 1), v.z & key_word_mask(wl, 2),
-                      v.w & key_word_mask(wl, 3));
-    }
-    pend_k[i] = key;
+  // Filter the lane's kPer samples of a step; a filter hit issues its L2
+  // screen load now and is resolved one step later (resolve()), so the L2
+  // round trip overlaps the next step's filtering instead of stalling.
+  __device__ __forceinline__ void filter(const uint4 (&v)[kPer], uint32_t lim) {
     const uint32_t lb = A.plan.l2_bits;
-    if (hit) {
-      if (lb) {
-        const uint32_t sb = screen_bit(key, lb);
-        pend_b[i] = sb & 31u;
-        pend_w[i] = __ldg(A.l2map + (sb >> 5));
-      } else {
-        pend_b[i] = 0;
-        pend_w[i] = 1u;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const uint32_t h = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
+      const bool hit = static_cast<uint32_t>(lane + 32 * i) < lim && admits(h);
+      cands32 += hit ? 1u : 0u;
+      uint32_t key = h;
+      if (!A.plan.key_gram) {
+        const uint32_t wl = A.plan.wkey_len;
+        key = key_words(v[i].x & key_word_mask(wl, 0), v[i].y & key_word_mask(wl, 1),
+                        v[i].z & key_word_mask(wl, 2), v[i].w & key_word_mask(wl, 3));
       }
+      pend_k[i] = key;
+      const uint32_t sb = lb ? screen_bit(key, lb) : 0u;
+      pend_b[i] = sb & 31u;
+      uint32_t w = 0;
+      if (hit) w = lb ? __ldg(A.l2map + (sb >> 5)) : 1u;
+      pend_w[i] = (A.plan.diag & 8) ? 0u : w;  // diagnostics: count only
     }
   }
 
   __device__ __forceinline__ void resolve() {
+    uint32_t surv = 0;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) push((pend_w[i] >> pend_b[i]) & 1u, pend_k[i], pend_pos + 512u * i);
-    pend_w[0] = pend_w[1] = 0;
+    for (int i = 0; i < kPer; ++i) surv |= ((pend_w[i] >> pend_b[i]) & 1u) << i;
+    if (__any_sync(kFull, surv != 0)) {
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 512u * i);
+    }
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) pend_w[i] = 0;
   }
 
-  __device__ __forceinline__ void process(const DirectDesc& d, const uint4& a, const uint4& b) {
+  __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer]) {
     const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
     if (flags & 1u) {
       fill = 0;
@@ -1230,8 +1236,7 @@ struct DirectScanner {
       resolve();  // the previous step of this slice
     }
     pend_pos = 16u * (d.t - pbase_t) + 16u * lane;
-    half(a, static_cast<uint32_t>(lane) < lim, 0);
-    half(b, static_cast<uint32_t>(lane) + 32 < lim, 1);
+    filter(v, lim);
     if (flags & 2u) {
       resolve();
       if (pqn) flush();
@@ -1251,13 +1256,18 @@ struct DirectScanner {
       if (!(d.lim_flags & 0x400u)) break;  // steps are issued in order: first invalid = end
       mbar_wait(bars + j, (phase >> j) & 1u);
       phase ^= 1u << j;
-      const uint4 a = slots[j * kDirectStep + lane];
-      const uint4 b = slots[j * kDirectStep + 32 + lane];
+      uint4 v[kPer];
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) v[i] = slots[j * kDirectStep + 32 * i + lane];
+      // the slot's shared-memory reads must have completed before the TMA
+      // refill below overwrites it: wait for the loaded values here
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) asm volatile("" ::"r"(v[i].x));
       __syncwarp();
       produce(j);  // refill the slot just read
       __syncwarp();
-      process(d, a, b);
-      j = (j + 1) & (kDirectDepth - 1);
+      process(d, v);
+      j = j + 1 == kDirectDepth ? 0 : j + 1;
     }
     unsigned long long c = cands32;
 #pragma unroll
@@ -1268,6 +1278,8 @@ struct DirectScanner {
 
 template <int H>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
+  // let the dependent gather grid launch early (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
   const size_t tbytes = align16(A.plan.table_bytes);
   {
@@ -1335,6 +1347,10 @@ __global__ void __launch_bounds__(1024) mag_compact_kernel(const __grid_constant
   __shared__ unsigned long long red[32];
   __shared__ unsigned long long s_pre[1024];
   __shared__ uint32_t s_cnt[1024];
+  // launched with programmatic stream serialization: wait for the scan grid
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (blockIdx.x == 0 && A.reset)
+    for (uint32_t i = threadIdx.x; i < A.reset_words; i += blockDim.x) A.reset[i] = 0;
   const uint64_t ns = A.num_slices;
   const uint64_t per = (ns + gridDim.x - 1) / gridDim.x;
   uint64_t s0 = blockIdx.x * per;
@@ -1343,7 +1359,24 @@ __global__ void __launch_bounds__(1024) mag_compact_kernel(const __grid_constant
   if (s1 > ns) s1 = ns;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
   unsigned long long acc = 0;
-  for (uint64_t i = tid; i < s0; i += blockDim.x) acc += A.slice_count[i];
+  {
+    // sum of every earlier slice: 16-byte loads, 4 independent per round trip
+    const uint64_t s0v = s0 & ~3ull;
+    const uint4* cv = reinterpret_cast<const uint4*>(A.slice_count);
+    uint64_t i = tid;
+    for (; i + 3 * blockDim.x < s0v / 4; i += 4 * blockDim.x) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = cv[i + u * blockDim.x];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc += (unsigned long long)x[u].x + x[u].y + x[u].z + x[u].w;
+    }
+    for (; i < s0v / 4; i += blockDim.x) {
+      const uint4 x = cv[i];
+      acc += (unsigned long long)x.x + x.y + x.z + x.w;
+    }
+    if (tid < s0 - s0v) acc += A.slice_count[s0v + tid];
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
   if (lane == 0) red[wid] = acc;
@@ -1511,7 +1544,20 @@ cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
 
 cudaError_t launch_compact(const ScanArgs& a, uint64_t* out, uint64_t out_cap, cudaStream_t stream,
                            int grid) {
-  mag_compact_kernel<<<grid, 1024, 0, stream>>>(a, out, out_cap);
+  // programmatic dependent launch: the gather's CTAs are scheduled while the
+  // scan drains and wait in griddepcontrol.wait for its completion
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mag_compact_kernel, a, out, out_cap);
+  if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

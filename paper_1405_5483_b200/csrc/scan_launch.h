@@ -44,6 +44,8 @@ struct ScanArgs {
   uint32_t* slice_count;        // exact per-slice counts (even past slice_cap)
   unsigned long long* counters; // [1] candidates [2] matches [3] max slice count
   unsigned long long* ticket;   // slice ticket of this launch (zeroed)
+  unsigned long long* reset;    // compaction zeroes reset[0..reset_words) (next search's counters)
+  uint32_t reset_words;
 };
 
 struct LaunchShape {
