@@ -1193,12 +1193,19 @@ struct DirectScanner {
   // round trip overlaps the next step's filtering instead of stalling.
   __device__ __forceinline__ void filter(const uint4 (&v)[kPer], uint32_t lim) {
     const uint32_t lb = A.plan.l2_bits;
+    const bool count_only = A.plan.diag & 8;  // diagnostics: no screen / verification
+    uint32_t h[kPer];
+    bool hit[kPer];
+    // all lookups first (independent shared-memory loads in flight together)
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) h[i] = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) hit[i] = admits(h[i]);
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      const uint32_t h = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
-      const bool hit = static_cast<uint32_t>(lane + 32 * i) < lim && admits(h);
-      cands32 += hit ? 1u : 0u;
-      uint32_t key = h;
+      hit[i] = hit[i] && static_cast<uint32_t>(lane + 32 * i) < lim;
+      cands32 += hit[i] ? 1u : 0u;
+      uint32_t key = h[i];
       if (!A.plan.key_gram) {
         const uint32_t wl = A.plan.wkey_len;
         key = key_words(v[i].x & key_word_mask(wl, 0), v[i].y & key_word_mask(wl, 1),
@@ -1207,9 +1214,10 @@ struct DirectScanner {
       pend_k[i] = key;
       const uint32_t sb = lb ? screen_bit(key, lb) : 0u;
       pend_b[i] = sb & 31u;
+      // the screen word is only consumed by resolve() one step later
       uint32_t w = 0;
-      if (hit) w = lb ? __ldg(A.l2map + (sb >> 5)) : 1u;
-      pend_w[i] = (A.plan.diag & 8) ? 0u : w;  // diagnostics: count only
+      if (hit[i] && !count_only) w = lb ? __ldg(A.l2map + (sb >> 5)) : 1u;
+      pend_w[i] = w;
     }
   }
 
