@@ -273,3 +273,31 @@ def test_sharded_spans(mag, ref):
         offs = np.concatenate([x[0] for x in parts])
         pids = np.concatenate([x[1] for x in parts])
         assert np.array_equal(offs, want[0]) and np.array_equal(pids, want[1]), world
+
+
+def _full_digests():
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "full_digests.json")
+    with open(p) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_configs(mag, cfg):
+    """BASELINE.json configs at FULL size: the GPU match set's count and
+    sha256 equal the reference Aho–Corasick's (tests/golden/full_digests.json,
+    made by tests/golden/make_full_digests.py from oracle/_ref)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_full_digests import input_digest, match_digest
+    from paper_1405_5483_b200 import workloads
+    want = _full_digests()[str(cfg)]
+    w = workloads.generate(cfg, 1.0)
+    assert input_digest(w) == {k: want[k] for k in ("text_sha256", "patterns_sha256")}
+    e = mag.Engine(w.patterns)
+    m = e.search(w.text)
+    offs, pids = m.arrays()
+    assert offs.size == want["matches"], (cfg, e.plan())
+    assert match_digest(offs, pids) == want["matches_sha256"], (cfg, e.plan())
