@@ -587,7 +587,8 @@ MAG_API mag_status mag_engine_get_info(const mag_engine* e, mag_engine_info* out
 MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) {
   if (!e || !out) return fail(MAG_ERR_NULL_ARGUMENT, "engine / out is NULL");
   const Plan& P = e->plan;
-  out->variant = P.variant;
+  // the machine that runs: mag may be planned onto the overlapping scan
+  out->variant = P.sp.overlapping ? MAG_VARIANT_SHIFTOR_OG : P.variant;
   out->gram_mode = P.sp.gram_mode;
   out->q = static_cast<int>(P.sp.q);
   out->k = static_cast<int>(P.sp.k);

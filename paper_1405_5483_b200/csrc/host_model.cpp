@@ -406,8 +406,9 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.sigma_prime = 256;
     // shared memory left for table + prefilter once the warp rings (of a
     // given chunk size) are in
-    auto room_for = [&](unsigned q, unsigned k, unsigned mp, int va, uint32_t chunk) {
+    auto room_for = [&](unsigned q, unsigned k, unsigned mp, int va, uint32_t chunk, int og = -1) {
       Plan probe = *P;
+      if (og >= 0) probe.sp.overlapping = og;
       probe.sp.q = q;
       probe.sp.k = k;
       probe.sp.m_prime = mp;
@@ -427,8 +428,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       int direct = 0;
       uint32_t blocks = 0;
       bool va = true;
+      int og = 0;
       double cpb = 1;
     } best;
+    best.og = sp.overlapping;
     auto pf_bytes = [](unsigned pf) { return pf ? align16((size_t(1) << pf) / 8) : size_t(16); };
     // verify-all baseline
     for (unsigned pf : kPf) {
@@ -448,34 +451,37 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         break;  // largest chunk that fits
       }
     }
-    if (rq.table_bits >= 0) {
-      const unsigned qmax = sp.overlapping ? static_cast<unsigned>(std::min<size_t>(16, m))
+    // machines: the requested variant's, and for mag (whose result set is
+    // parameter-invariant) also the overlapping one (q-gram per byte, window 1)
+    const int og_lo = rq.variant == 2 ? 1 : 0, og_hi = rq.variant == 1 ? 0 : 1;
+    for (int og = og_lo; og <= og_hi && rq.table_bits >= 0; ++og) {
+      const unsigned qmax = og ? static_cast<unsigned>(std::min<size_t>(16, m))
                                            : static_cast<unsigned>(std::min<size_t>(16, (m + 1) / 2));
       for (unsigned q = 1; q <= qmax; ++q) {
         if (rq.q > 0 && q != static_cast<unsigned>(rq.q)) continue;
-        const size_t L = sp.overlapping ? m - q + 1 : (m - q + 1) / q;
+        const size_t L = og ? m - q + 1 : (m - q + 1) / q;
         if (L < 1) continue;
         const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
-        const unsigned kmax = sp.overlapping ? 1 : static_cast<unsigned>(std::min<size_t>(L, w));
+        const unsigned kmax = og ? 1 : static_cast<unsigned>(std::min<size_t>(L, w));
         for (unsigned k = 1; k <= kmax; ++k) {
-          if (rq.k > 0 && !sp.overlapping && k != static_cast<unsigned>(rq.k)) continue;
+          if (rq.k > 0 && !og && k != static_cast<unsigned>(rq.k)) continue;
           const unsigned mpmax = static_cast<unsigned>(std::min<size_t>(L / k, w / k));
           for (unsigned mp = 1; mp <= mpmax; ++mp) {
             const unsigned el = pow2ceil_log2(std::max(1u, k * mp));
             const double sample_cost = (kCostSample + (mp - 1) * kCostShift) /
-                                       (sp.overlapping ? 1.0 : static_cast<double>(k * q));
-            const bool wkey = !sp.overlapping && q > 1;
+                                       (og ? 1.0 : static_cast<double>(k * q));
+            const bool wkey = !og && q > 1;
             const double nkeys = wkey ? keys * q : keys;
             const double hits = key_hits(nkeys, sigma_obs,
                                          static_cast<unsigned>(wkey ? std::min<size_t>(16, m - q + 1)
                                                                     : std::min<size_t>(16, m)));
             for (unsigned tbits = 12; tbits <= 24; ++tbits) {
              if (rq.table_bits > 0 && tbits != static_cast<unsigned>(rq.table_bits)) continue;
-             const unsigned hmax = (!sp.overlapping && mp == 1 && k == 1 && tbits >= 8) ? 4 : 1;
+             const unsigned hmax = (mp == 1 && k == 1 && tbits >= 8) ? 4 : 1;
              for (unsigned H = 1; H <= hmax; ++H) {
               if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
               const size_t tbytes = align16((size_t(1) << (tbits + el)) / 8);
-              const double adm = sp.overlapping ? keys : keys * q;
+              const double adm = og ? keys : keys * q;
               double p = est_position_p(adm, universe, std::ldexp(1.0, static_cast<int>(tbits)));
               if (H > 1) {  // probes inside a 32-entry block (est. as a plain Bloom filter)
                 const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
@@ -485,19 +491,19 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
               }
               const double pm = std::pow(p, static_cast<double>(mp));
               // candidates per byte, and verified starts per byte
-              const double cpb = sp.overlapping ? pm : pm / q;
+              const double cpb = og ? pm : pm / q;
               for (unsigned pf : kPf) {
                 uint32_t chunk = 0;
                 for (uint32_t c : kChunks) {
                   if (rq.tile_bytes > 0 && c != kChunks[0]) break;
-                  if (tbytes + pf_bytes(pf) <= room_for(q, k, mp, 0, c)) {
+                  if (tbytes + pf_bytes(pf) <= room_for(q, k, mp, 0, c, og)) {
                     chunk = c;
                     break;
                   }
                 }
                 if (!chunk) continue;
                 const double fp = pf ? prefilter_fp(nkeys, pf) : 1.0;
-                double cost = sample_cost + (H - 1) * kCostProbeBit / (k * q) + kCostChunk / chunk;
+                double cost = sample_cost + (H - 1) * kCostProbeBit / (og ? 1.0 : static_cast<double>(k * q)) + kCostChunk / chunk;
                 if (wkey)  // window keys: one batched key + L2 screen per candidate
                   cost += cpb * (kCostCand + kCostWindow + (pf ? kCostPf : 0.0) +
                                  fp * (kCostScreen + 0.01 * kCostProbe) + hits * kCostCompare);
@@ -513,6 +519,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                   best.pf = pf;
                   best.chunk = chunk;
                   best.va = false;
+                  best.og = og;
                   best.cpb = cpb;
                 }
               }
@@ -561,11 +568,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.va = false;
           best.cpb = cpb;
           best.direct = 1;
+          best.og = 0;
           best.blocks = H > 1 ? blocks : 0;
           best.tb = H > 1 ? 0 : tb1;
         }
       }
     }
+    sp.overlapping = best.og;
     if (best.va) {
       sp.q = 1;
       sp.k = 1;

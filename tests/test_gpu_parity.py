@@ -120,7 +120,7 @@ def test_hashed_counters_match_port(mag, ref, port):
         if pl["verify_all"]:
             assert met.candidates == met.filter_reads
             continue
-        P = port.params(variant=0 if variant == "mag" else 2, gram_mode=1, q=pl["q"], k=pl["k"],
+        P = port.params(variant=0 if pl["variant"] == 0 else 2, gram_mode=1, q=pl["q"], k=pl["k"],
                         table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
                         blocks=pl["blocks"])
         o, p, reads, cands = port.search(text, pats, P)
@@ -212,7 +212,9 @@ def test_baseline_configs_reduced(mag, ref, cfg, scale):
     m = e.search(w.text)
     offs, pids = m.arrays()
     assert np.array_equal(offs, want[0]) and np.array_equal(pids, want[1]), (cfg, e.plan())
-    assert m.metrics().filter_reads == (w.text.size // e.info().q) // e.info().k or e.plan()["verify_all"]
+    pl, n = e.plan(), w.text.size
+    want_reads = n if pl["verify_all"] else (n - pl["q"] + 1 if pl["variant"] == 2 else (n // pl["q"]) // pl["k"])
+    assert m.metrics().filter_reads == want_reads
 
 
 def _golden():
