@@ -34,7 +34,16 @@ typedef struct mag_options_ex {
   int stages;      /* TMA ring depth, 0 = auto */
   int device;      /* CUDA device ordinal, -1 = current */
   int probes;      /* hashed: table entries probed per gram, 0 = auto */
+  int scan_kernel; /* mag_scan_kernel: which scan the planner may pick, 0 = auto */
 } mag_options_ex;
+
+/* Scan kernels of hashed plans (mag_options_ex.scan_kernel). */
+typedef enum mag_scan_kernel {
+  MAG_KERNEL_AUTO = 0,
+  MAG_KERNEL_STAGED = 1, /* TMA-staged strided / overlapping machine (every plan shape) */
+  MAG_KERNEL_DIRECT = 2, /* q = 16 aligned-sample stream + L2 screen (m >= 31) */
+  MAG_KERNEL_ROLL = 3    /* dense rolling-hash prefix Bloom scan (m >= 8) */
+} mag_scan_kernel;
 
 MAG_API void mag_options_ex_init(mag_options_ex* opts);
 MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns,
@@ -61,6 +70,7 @@ typedef struct mag_plan_info {
   uint32_t probes;      /* hashed, m' = k = 1: table entries probed per gram */
   uint32_t blocks;      /* probes >= 2: 64-entry table blocks */
   int direct;           /* q = 16 stream kernel */
+  int roll;             /* dense rolling-hash scan (every position, q-byte prefix Bloom) */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

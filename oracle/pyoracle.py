@@ -319,3 +319,53 @@ class Port:
 
 def as_pairs(offs, pids):
     return list(zip([int(x) for x in offs], [int(x) for x in pids]))
+
+
+# ---------------------------------------------------------------- roll --
+# Restatement of the GPU's dense rolling-hash filter (a GPU extension, not a
+# reference algorithm: paper_1405_5483_b200/csrc/mag_common.h roll_*), used
+# to check the roll kernel's Bloom table and its candidate counter.
+ROLL_B = 0x9E3779B1
+ROLL_MIX = 0x2C1B3C6D
+
+
+def roll_hashes(text, q: int) -> np.ndarray:
+    """H(p) = sum_{j<q} t[p+j] * B^(q-1-j) mod 2^32 for every p <= n - q."""
+    t = _u8(text).astype(np.uint32)
+    n = t.size - q + 1
+    if n <= 0:
+        return np.zeros(0, dtype=np.uint32)
+    h = np.zeros(n, dtype=np.uint32)
+    with np.errstate(over="ignore"):
+        for j in range(q):
+            h = h * np.uint32(ROLL_B) + t[j:j + n]
+    return h
+
+
+def _roll_slots(h: np.ndarray, words: int, probes: int):
+    with np.errstate(over="ignore"):
+        g = h.astype(np.uint32) * np.uint32(ROLL_MIX)
+    w = ((g.astype(np.uint64) * np.uint64(words)) >> np.uint64(32)).astype(np.int64)
+    bits = [((g >> np.uint32(5 * i)) & np.uint32(31)).astype(np.uint32) for i in range(probes)]
+    return w, bits
+
+
+def roll_bloom(patterns, q: int, words: int, probes: int) -> np.ndarray:
+    """The Bloom words the host builds (bit set = present)."""
+    keys = np.array([roll_hashes(p[:q], q)[0] for p in patterns], dtype=np.uint32)
+    w, bits = _roll_slots(keys, words, probes)
+    out = np.zeros(words, dtype=np.uint32)
+    for b in bits:
+        np.bitwise_or.at(out, w, np.uint32(1) << b)
+    return out
+
+
+def roll_candidates(text, patterns, q: int, words: int, probes: int) -> int:
+    """Positions p <= n - q whose rolling hash passes the Bloom filter."""
+    table = roll_bloom(patterns, q, words, probes)
+    h = roll_hashes(text, q)
+    w, bits = _roll_slots(h, words, probes)
+    ok = np.ones(h.size, dtype=bool)
+    for b in bits:
+        ok &= ((table[w] >> b) & np.uint32(1)).astype(bool)
+    return int(ok.sum())

@@ -40,6 +40,8 @@ MAPPING_AUTO, MAPPING_IDENTITY, MAPPING_FREQUENCY, MAPPING_BALANCED, MAPPING_LOW
 MAPPINGS = {"auto": -1, "identity": 0, "freq": 1, "balance": 2, "lowbits": 3}
 # mag_gram_mode (mag_b200.h)
 GRAM_AUTO, GRAM_EXACT, GRAM_HASHED = -1, 0, 1
+# mag_scan_kernel (mag_b200.h)
+KERNELS = {"auto": 0, "staged": 1, "direct": 2, "roll": 3}
 
 
 class MagError(RuntimeError):
@@ -61,7 +63,7 @@ class _OptionsEx(C.Structure):  # mag_b200.h
     _fields_ = [
         ("base", _Options), ("gram_mode", C.c_int), ("table_bits", C.c_int),
         ("word_bits", C.c_int), ("tile_bytes", C.c_int), ("warps", C.c_int),
-        ("stages", C.c_int), ("device", C.c_int), ("probes", C.c_int),
+        ("stages", C.c_int), ("device", C.c_int), ("probes", C.c_int), ("scan_kernel", C.c_int),
     ]
 
 
@@ -81,7 +83,7 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("bucket_bits", C.c_uint32), ("tile_bytes", C.c_uint32), ("halo", C.c_uint32),
         ("warps", C.c_uint32), ("stages", C.c_uint32), ("smem_bytes", C.c_size_t),
         ("predicted_candidates_per_byte", C.c_double), ("probes", C.c_uint32),
-        ("blocks", C.c_uint32), ("direct", C.c_int),
+        ("blocks", C.c_uint32), ("direct", C.c_int), ("roll", C.c_int),
     ]
 
 
@@ -286,13 +288,14 @@ class Engine:
     Keyword options mirror ``mag_options`` (variant, mapping, lowbits, q, k,
     sigma_prime, threads, histogram_sample) plus the GPU extras of
     ``mag_options_ex`` (gram_mode, table_bits, word_bits, tile_bytes, warps,
-    stages, device; device=-2 builds the host tables only, no upload).
+    stages, device, probes, scan_kernel; device=-2 builds the host tables
+    only, no upload).
     """
 
     def __init__(self, patterns: Sequence[bytes], variant="mag", mapping="auto", lowbits=0, q=0, k=0,
                  sigma_prime=0, threads=1, histogram_sample: Optional[bytes] = None,
                  gram_mode=GRAM_AUTO, table_bits=0, word_bits=0, tile_bytes=0, warps=0, stages=0,
-                 device=-1, probes=0):
+                 device=-1, probes=0, scan_kernel="auto"):
         L = lib()
         self._h = C.c_void_p()
         opts = _OptionsEx()
@@ -309,6 +312,7 @@ class Engine:
         opts.gram_mode, opts.table_bits, opts.word_bits = int(gram_mode), int(table_bits), int(word_bits)
         opts.tile_bytes, opts.warps, opts.stages, opts.device = int(tile_bytes), int(warps), int(stages), int(device)
         opts.probes = int(probes)
+        opts.scan_kernel = KERNELS[scan_kernel] if isinstance(scan_kernel, str) else int(scan_kernel)
         bufs = [_as_u8(p) for p in patterns]
         n = len(bufs)
         ptrs = (C.POINTER(C.c_uint8) * max(n, 1))(*[_u8ptr(b) for b in bufs])

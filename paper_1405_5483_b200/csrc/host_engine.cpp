@@ -524,6 +524,9 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     rq.warps = opts.warps;
     rq.stages = opts.stages;
     rq.probes = opts.probes;
+    rq.kernel = opts.scan_kernel;
+    if (opts.scan_kernel < 0 || opts.scan_kernel > 3)
+      return fail(MAG_ERR_BAD_CONFIG, "unknown scan kernel " + std::to_string(opts.scan_kernel));
     if (opts.base.q < 0 || opts.base.k < 0 || opts.base.sigma_prime < 0)
       return fail(MAG_ERR_BAD_CONFIG, "q, k and sigma' must be >= 0 (0 = auto)");
     if (opts.base.mapping < -1 || opts.base.mapping > 3)
@@ -612,6 +615,7 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->probes = P.sp.probes;
   out->blocks = P.sp.blocks;
   out->direct = P.sp.direct;
+  out->roll = P.sp.roll;
   return MAG_OK;
 }
 

@@ -245,7 +245,10 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostChunk = 4800,  // per staged chunk (loader + bookkeeping), thread-instr
                  kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
                  kCostPf = 15,       // shared-memory prefilter test
-                 kCostDirectHit = 6;  // direct kernel: a filter hit issues one L2 screen load
+                 kCostDirectHit = 6,  // direct kernel: a filter hit issues one L2 screen load
+                 kCostRollPos = 17,   // roll kernel: roll + one Bloom word per position (2 probes)
+                 kCostRollProbe = 2,  // each further Bloom probe
+                 kCostRollCand = 90;  // expansion + start key + bucket walk of a Bloom hit
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -309,7 +312,7 @@ void set_entry_geometry(ScanPlan& sp) {
   uint64_t match = 0;
   for (unsigned j = 0; j < sp.k; ++j) match |= 1ull << (j * sp.m_prime + sp.m_prime - 1);
   sp.match_mask = match;
-  if (sp.probes > 1) sp.entries = static_cast<uint64_t>(sp.blocks) * 64;
+  if (sp.probes > 1 && !sp.roll) sp.entries = static_cast<uint64_t>(sp.blocks) * 64;
   const uint64_t tbits = sp.entries << sp.entry_log2;
   sp.table_bytes = align16(std::max<uint64_t>(16, (tbits + 7) / 8));
 }
@@ -345,6 +348,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   const size_t m = pd.m;
   const unsigned w = rq.word_bits > 0 ? std::min(64, rq.word_bits) : 64;
 
+  uint32_t best_halo = 0;  // roll plans: staged bytes past a step
   const bool reference_mode = rq.gram_mode == 0 ||
                               (rq.gram_mode < 0 && (rq.q || rq.k || rq.sigma_prime ||
                                                      rq.mapping != -1));
@@ -426,6 +430,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       unsigned q = 1, k = 1, mp = 1, tb = 0, pf = 0, H = 1;
       uint32_t chunk = kChunkTarget;
       int direct = 0;
+      int roll = 0;
+      uint32_t roll_words = 0, halo = 0;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -433,8 +439,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     } best;
     best.og = sp.overlapping;
     auto pf_bytes = [](unsigned pf) { return pf ? align16((size_t(1) << pf) / 8) : size_t(16); };
+    const bool allow_staged = rq.kernel == 0 || rq.kernel == 1;
     // verify-all baseline
     for (unsigned pf : kPf) {
+      if (!allow_staged) break;
       for (uint32_t chunk : kChunks) {
         if (rq.tile_bytes > 0 && chunk != kChunks[0]) break;
         if (pf_bytes(pf) > room_for(1, 1, 1, 1, chunk)) continue;
@@ -454,7 +462,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     // machines: the requested variant's, and for mag (whose result set is
     // parameter-invariant) also the overlapping one (q-gram per byte, window 1)
     const int og_lo = rq.variant == 2 ? 1 : 0, og_hi = rq.variant == 1 ? 0 : 1;
-    for (int og = og_lo; og <= og_hi && rq.table_bits >= 0; ++og) {
+    for (int og = og_lo; og <= og_hi && rq.table_bits >= 0 && allow_staged; ++og) {
       const unsigned qmax = og ? static_cast<unsigned>(std::min<size_t>(16, m))
                                            : static_cast<unsigned>(std::min<size_t>(16, (m + 1) / 2));
       for (unsigned q = 1; q <= qmax; ++q) {
@@ -530,7 +538,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       }
     }
     // direct q = 16 stream kernel: no staging, the table takes the smem
-    if (rq.table_bits >= 0 && !sp.overlapping && m >= 31 && (rq.q == 0 || rq.q == 16) &&
+    if ((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 31 &&
+        (rq.q == 0 || rq.q == 16) &&
         rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0) {
       const unsigned q = 16;
       const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
@@ -574,6 +583,52 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         }
       }
     }
+    // dense rolling-hash scan: every position, whole-prefix (q <= m) keys in a
+    // shared-memory Bloom filter; for pattern sets that saturate gram filters
+    if ((rq.kernel == 0 || rq.kernel == 3) && rq.table_bits >= 0 && rq.variant != 1 && m >= 8 &&
+        rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0) {
+      static const unsigned kRollQ[] = {32, 24, 20, 16, 12, 8};
+      unsigned q = 0;
+      for (unsigned c : kRollQ)
+        if (c <= m && (rq.q == 0 || static_cast<unsigned>(rq.q) == c)) {
+          q = c;
+          break;
+        }
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+      const uint32_t v4 = (32 + q - 1 + 15) / 16;
+      const uint32_t halo = static_cast<uint32_t>(
+          align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
+      const size_t fixed = roll_smem(0, halo, warps) + 1024;
+      const uint32_t words =
+          rq.smem_limit > fixed ? static_cast<uint32_t>((rq.smem_limit - fixed) / 16 * 4) : 0;
+      const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
+      const double exact = universe > 1e15 ? 0.0 : std::min(1.0, keys / universe);
+      for (unsigned H = 2; q && words >= 1024 && H <= 3; ++H) {
+        if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
+        const double bits = 32.0 * words;
+        const double fill = 1.0 - std::exp(-static_cast<double>(H) * keys / bits);
+        const double fp = std::min(1.0, 1.4 * std::pow(fill, static_cast<double>(H)));  // blocked penalty
+        const double cpb = exact + (1.0 - exact) * fp;
+        const double cost = kCostRollPos + (H - 2) * kCostRollProbe + cpb * kCostRollCand;
+        if (cost < best.cost * 0.999) {
+          best = Cand{};
+          best.cost = cost;
+          best.q = q;
+          best.H = H;
+          best.va = false;
+          best.og = 1;
+          best.cpb = cpb;
+          best.roll = 1;
+          best.roll_words = words;
+          best.halo = halo;
+          best.chunk = kRollStep;
+        }
+      }
+    }
+    if (rq.kernel != 0 && !std::isfinite(best.cost)) {
+      *err = "the requested scan kernel cannot run this pattern set / option combination";
+      return kBadConfig;
+    }
     sp.overlapping = best.og;
     if (best.va) {
       sp.q = 1;
@@ -591,6 +646,14 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.probes = best.H;
       sp.blocks = best.H > 1 ? (best.direct ? best.blocks : static_cast<uint32_t>((1ull << best.tb) / 64)) : 0;
       sp.direct = best.direct;
+      sp.roll = best.roll;
+      best_halo = best.halo;
+      if (best.roll) {
+        sp.roll_words = best.roll_words;
+        sp.entries = static_cast<uint64_t>(best.roll_words) * 32;
+        sp.table_bits = 0;
+        sp.blocks = 0;
+      }
     }
     sp.pf_bits = best.pf;
     P->chunk_target = best.chunk;
@@ -624,6 +687,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.m_prime = static_cast<uint32_t>(std::min<size_t>(L / sp.k, w / sp.k));
   set_entry_geometry(sp);
   finish_geometry(pd, rq, P);
+  if (sp.roll) {  // roll kernel geometry: 2 KiB steps, 16 steps per slice
+    P->chunk_samples = kRollStep;
+    P->slice_samples = static_cast<uint64_t>(kRollStep) * 16;
+    P->back = best_halo;
+    P->ring = kRollDepth;
+    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+  }
 
   // ---- shared-memory placement
   const size_t fixed = fixed_smem(*P);
@@ -668,6 +738,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
 
 size_t plan_smem(const Plan& p) {
   if (p.sp.direct) return direct_smem(p.sp, p.nwarps);
+  if (p.sp.roll) return roll_smem(p.sp.roll_words, p.back, p.nwarps);
   return smem_layout(p.sp, p.slot_bytes, p.ring, p.nwarps).total;
 }
 
@@ -719,6 +790,16 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
   table->assign(sp.table_bytes, 0xff);
   if (sp.verify_all) {
     table->assign(sp.table_bytes, 0);
+    return;
+  }
+  if (sp.roll) {  // Bloom words of the patterns' q-byte prefix hashes (bit set = present)
+    table->assign(sp.table_bytes, 0);
+    uint32_t* w = reinterpret_cast<uint32_t*>(table->data());
+    for (size_t i = 0; i < pd.r; ++i) {
+      const uint32_t g = roll_hash_bytes(pd.pattern(i), sp.q) * kRollMix;
+      const uint32_t wi = roll_word(g, sp.roll_words);
+      for (unsigned j = 0; j < sp.probes; ++j) w[wi] |= 1u << ((g >> (5 * j)) & 31u);
+    }
     return;
   }
   const size_t m = pd.m;

@@ -69,6 +69,27 @@ MAG_HD uint32_t bloom_block(uint32_t h, uint32_t blocks) {
 MAG_HD uint64_t bloom_mix(uint32_t h) { return static_cast<uint64_t>(h) * 0x9E3779B97F4A7C15ull; }
 MAG_HD uint32_t bloom_bit(uint64_t g, unsigned i) { return static_cast<uint32_t>(g >> (58 - 6 * i)) & 63u; }
 
+// Rolling q-gram hash of the dense (roll) scan: H(p) = sum_{j<q} t[p+j] *
+// B^(q-1-j) mod 2^32, so H(p+1) = H(p)*B + t[p+q] - t[p]*B^q (two IMADs per
+// position).  Its filter is a blocked Bloom filter of 32-bit words: word
+// umulhi(g, words), bits (g >> 5i) & 31 for i < probes, g = H * kRollMix.
+constexpr uint32_t kRollB = 0x9E3779B1u;
+constexpr uint32_t kRollMix = 0x2C1B3C6Du;
+constexpr int kRollMaxProbes = 4;
+MAG_HD uint32_t roll_hash_bytes(const uint8_t* p, unsigned q) {
+  uint32_t h = 0;
+  for (unsigned i = 0; i < q; ++i) h = h * kRollB + p[i];
+  return h;
+}
+MAG_HD uint32_t roll_pow(unsigned q) {
+  uint32_t x = 1;
+  for (unsigned i = 0; i < q; ++i) x *= kRollB;
+  return x;
+}
+MAG_HD uint32_t roll_word(uint32_t g, uint32_t words) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(g) * words) >> 32);
+}
+
 // Verification key: the first v = min(m, 16) bytes of a start, read as four
 // little-endian words (bytes past v zeroed), mixed.  Top bits index the
 // shared-memory prefilter, low bits the bucket table.
@@ -120,6 +141,8 @@ struct ScanPlan {
   uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..kMaxProbes)
   uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
   int direct;             // q = 16 stream kernel (register prefetch, no staging)
+  int roll;               // dense rolling-hash scan: every position, q-gram Bloom
+  uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
   uint32_t entry_log2;    // log2(bits per mask entry), 0..6
   uint64_t entries;       // number of mask entries
   uint64_t table_bytes;   // packed table size (multiple of 16)
@@ -178,6 +201,16 @@ constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lan
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
          size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * (16 + 8) + 64;
+}
+
+// Roll kernel: Bloom words, per-warp ring of kRollDepth slots of
+// kRollStep text bytes + halo (+ mbarriers and step descriptors).
+constexpr int kRollDepth = 3;
+constexpr int kRollStep = 2048;   // positions per step: 2 runs of 32 per lane
+MAG_HD uint32_t roll_slot_bytes(uint32_t halo) { return static_cast<uint32_t>(align16(kRollStep + halo)); }
+MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
+  return align16(size_t(words) * 4) + size_t(nwarps) * kRollDepth * roll_slot_bytes(halo) +
+         size_t(nwarps) * kRollDepth * (32 + 8) + 64;
 }
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,

@@ -1342,6 +1342,334 @@ cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
   }
 }
 
+// ============================================================== roll kernel
+// Dense scan for pattern sets whose q-grams saturate any strided filter
+// (many short patterns, e.g. r = 100k, m = 12 over DNA): every text
+// position p is a sample whose key is the rolling hash H(p) of the q-byte
+// pattern prefix (mag_common.h roll_*), tested against a blocked Bloom
+// filter resident in shared memory — one 32-bit word and `H` bit tests per
+// position, two IMADs to roll.  Each warp streams steps of kRollStep bytes
+// (+ halo) through a kRollDepth-slot TMA ring; lane l owns the runs
+// [1024 r + 32 l, +32) of a step (two independent rolling chains per lane).
+// Hits of a run form a 32-bit mask per lane; they are expanded in text order
+// (warp prefix over the masks) and verified while the step is still staged:
+// start key of the candidate's first min(m,16) bytes -> bucket walk ->
+// byte compare against the staged text.  Output: per-slice ordered staging,
+// as every other scan kernel (mag_compact_kernel gathers).
+struct __align__(16) RollDesc {
+  unsigned long long t;  // first position (= byte offset) of the step
+  uint32_t slice;
+  uint32_t lim_flags;    // valid positions | flags << 16 (1 first, 2 last, 4 live)
+  uint32_t valid;        // staged bytes
+  uint32_t pad[3];
+};
+
+template <int Q, int H>
+struct RollScanner {
+  static constexpr int kRun = 32;                  // positions per lane run
+  static constexpr int kBytes = kRun + Q - 1;      // bytes one run reads
+  static constexpr int kV4 = (kBytes + 15) / 16;   // 16-byte loads per run
+  static constexpr int kW = kV4 * 4;
+  const ScanArgs& A;
+  const int lane;
+  const uint32_t* bloom;
+  uint8_t* slots;
+  uint64_t* bars;
+  RollDesc* desc;
+  const uint32_t slot_bytes;
+  const uint32_t bq;        // B^Q
+  uint32_t fill, cands32;
+  uint64_t* out;
+  // producer cursor (warp-uniform)
+  unsigned long long p_t, p_end;
+  uint32_t p_slice;
+  bool p_done, p_first;
+
+  __device__ RollScanner(const ScanArgs& a, const uint32_t* bl, uint8_t* sl, uint64_t* b, RollDesc* d, int l)
+      : A(a), lane(l), bloom(bl), slots(sl), bars(b), desc(d), slot_bytes(roll_slot_bytes(a.back)),
+        bq(roll_pow(Q)), fill(0), cands32(0), out(nullptr), p_t(0), p_end(0), p_slice(0), p_done(false),
+        p_first(false) {}
+
+  // Claim (if needed) and stage the next step into slot j.
+  __device__ __forceinline__ void produce(int j) {
+    while (!p_done && p_t >= p_end) {
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(A.ticket, 1ull);
+      x = __shfl_sync(kFull, x, 0) + A.slice_begin;
+      if (x >= A.slice_end) {
+        p_done = true;
+        break;
+      }
+      const unsigned long long t0 = x * A.slice_samples;
+      const unsigned long long t1 = t0 + A.slice_samples < A.samples ? t0 + A.slice_samples : A.samples;
+      if (t1 <= t0) {
+        if (lane == 0) A.slice_count[x] = 0;
+        continue;
+      }
+      p_slice = static_cast<uint32_t>(x);
+      p_t = t0;
+      p_end = t1;
+      p_first = true;
+    }
+    uint8_t* dst = slots + static_cast<size_t>(j) * slot_bytes;
+    if (p_done) {
+      if (lane == 0) desc[j].lim_flags = 0;
+      __syncwarp();
+      return;
+    }
+    const uint32_t lim = p_end - p_t < static_cast<unsigned long long>(kRollStep)
+                             ? static_cast<uint32_t>(p_end - p_t) : static_cast<uint32_t>(kRollStep);
+    const unsigned long long hi = p_t + slot_bytes < A.n ? p_t + slot_bytes : A.n;
+    const uint32_t valid = static_cast<uint32_t>(hi - p_t);
+    const uint32_t bulk = valid & ~15u;
+    if (static_cast<uint32_t>(lane) < valid - bulk) dst[bulk + lane] = __ldg(A.text + p_t + bulk + lane);
+    __syncwarp();
+    if (lane == 0) {
+      RollDesc& d = desc[j];
+      d.t = p_t;
+      d.slice = p_slice;
+      d.valid = valid;
+      d.lim_flags = lim | ((4u | (p_first ? 1u : 0u) | (p_t + lim >= p_end ? 2u : 0u)) << 16);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(bars + j, bulk);
+      if (bulk) tma_load_1d_stream(dst, A.text + p_t, bulk, bars + j, policy_evict_first());
+    }
+    __syncwarp();
+    p_t += lim;
+    p_first = false;
+  }
+
+  static __device__ __forceinline__ uint32_t byte_at(const uint32_t (&w)[kW], int k) {
+    return __byte_perm(w[k >> 2], 0u, 0x4440u | static_cast<uint32_t>(k & 3));
+  }
+
+  __device__ __forceinline__ uint32_t test(uint32_t h) const {
+    const uint32_t g = h * kRollMix;
+    const uint32_t wd = bloom[roll_word(g, A.plan.roll_words)];
+    uint32_t r = __funnelshift_r(wd, wd, g);
+#pragma unroll
+    for (int i = 1; i < H; ++i) r &= __funnelshift_r(wd, wd, g >> (5 * i));
+    return r & 1u;
+  }
+
+  // Bloom hits of the lane's run starting at slot offset `base` (32 positions).
+  __device__ __forceinline__ uint32_t filter_run(const uint8_t* sb, int base) const {
+    uint32_t w[kW];
+    const uint4* src = reinterpret_cast<const uint4*>(sb + base);
+#pragma unroll
+    for (int v = 0; v < kV4; ++v) {
+      const uint4 x = src[v];
+      w[4 * v] = x.x;
+      w[4 * v + 1] = x.y;
+      w[4 * v + 2] = x.z;
+      w[4 * v + 3] = x.w;
+    }
+    uint32_t h = 0;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) h = h * kRollB + byte_at(w, k);
+    uint32_t hits = test(h);
+#pragma unroll
+    for (int i = 1; i < kRun; ++i) {
+      h = h * kRollB + (byte_at(w, i + Q - 1) - byte_at(w, i - 1) * bq);
+      hits |= test(h) << i;
+    }
+    return hits;
+  }
+
+  // Start key (first key_len bytes) at slot offset pr.
+  __device__ __forceinline__ uint32_t key_at(const uint32_t* sw, uint32_t pr) const {
+    const uint32_t wi = pr >> 2, sh = (pr & 3u) << 3, v = A.plan.key_len;
+    uint32_t x[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) x[k] = sw[wi + k];
+    return key_words(__funnelshift_r(x[0], x[1], sh) & key_word_mask(v, 0),
+                     __funnelshift_r(x[1], x[2], sh) & key_word_mask(v, 1),
+                     __funnelshift_r(x[2], x[3], sh) & key_word_mask(v, 2),
+                     __funnelshift_r(x[3], x[4], sh) & key_word_mask(v, 3));
+  }
+
+  // Pattern pid (len bytes) against the staged text at slot offset pr.
+  __device__ bool equal_slot(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
+                             uint32_t pid, uint32_t len) const {
+    if (pr + len + 4 > valid) return equal_text(A, a, pid, len);
+    const uint4* pv4 = reinterpret_cast<const uint4*>(A.pat_bytes + __ldg(A.pat_off + pid));
+    const uint32_t wi = pr >> 2, sh = (pr & 3u) << 3;
+    for (uint32_t i = 0; i < len; i += 16) {
+      const uint4 pv = __ldg(pv4 + (i >> 4));
+      const uint32_t pw[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t o = i + 4 * j;
+        if (o >= len) break;
+        const uint32_t tw = __funnelshift_r(sw[wi + (o >> 2)], sw[wi + (o >> 2) + 1], sh);
+        const uint32_t rem = len - o;
+        const uint32_t msk = rem >= 4 ? 0xffffffffu : ((1u << (8 * rem)) - 1u);
+        if ((tw ^ pw[j]) & msk) return false;
+      }
+    }
+    return true;
+  }
+
+  // Matches at slot offset pr: counted (first pid kept), or written from dst[idx].
+  __device__ uint32_t probe(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
+                            uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first) const {
+    const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
+    const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
+    uint32_t c = 0;
+    for (uint32_t e = lo; e < hi; ++e) {
+      const uint2 ent = __ldg(A.bucket_entries + e);
+      if (ent.x != key) continue;
+      const uint32_t len = __ldg(A.pat_len + ent.y);
+      if (a + len > A.n || !equal_slot(sw, valid, a, pr, ent.y, len)) continue;
+      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, ent.y);
+      if (c == 0 && first) *first = ent.y;
+      ++c;
+    }
+    return c;
+  }
+
+  // Expand and verify the hits of one run (lane masks, text order).
+  __device__ void verify_run(const uint32_t* sw, uint32_t valid, unsigned long long t, int run_base,
+                             uint32_t hits) {
+    const uint32_t cnt = __popc(hits);
+    const uint32_t excl = warp_excl_scan(cnt, lane);
+    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
+    cands32 += cnt;
+    if (A.plan.diag & 8) return;
+    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
+      const uint32_t rank = r0 + lane;
+      const bool live = rank < total;
+      int o = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const uint32_t e = __shfl_sync(kFull, excl, o + step);
+        if (e <= rank) o += step;
+      }
+      const uint32_t hm = __shfl_sync(kFull, hits, o);
+      const uint32_t eo = __shfl_sync(kFull, excl, o);
+      uint32_t c = 0, pid0 = 0, key = 0, pr = 0;
+      unsigned long long a = 0;
+      if (live) {
+        pr = static_cast<uint32_t>(run_base + 32 * o + static_cast<int>(__fns(hm, 0, static_cast<int>(rank - eo) + 1)));
+        a = t + pr;
+        key = key_at(sw, pr);
+        c = probe(sw, valid, a, pr, key, nullptr, 0, &pid0);
+      }
+      if (!__any_sync(kFull, c != 0)) continue;
+      const uint32_t ex = warp_excl_scan(c, lane);
+      const uint32_t tot = __shfl_sync(kFull, ex + c, 31);
+      if (c == 1) {
+        if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(a, pid0);
+      } else if (c > 1) {
+        probe(sw, valid, a, pr, key, out, fill + ex, nullptr);
+      }
+      fill += tot;
+    }
+  }
+
+  __device__ void run() {
+#pragma unroll 1
+    for (int j = 0; j < kRollDepth; ++j) produce(j);
+    uint32_t phase = 0;
+    int j = 0;
+#pragma unroll 1
+    while (true) {
+      const RollDesc d = desc[j];
+      if (!(d.lim_flags & (4u << 16))) break;  // steps are issued in order: first dead slot = end
+      mbar_wait(bars + j, (phase >> j) & 1u);
+      phase ^= 1u << j;
+      const uint32_t lim = d.lim_flags & 0xffffu, flags = d.lim_flags >> 16;
+      if (flags & 1u) {
+        fill = 0;
+        out = A.staging + static_cast<size_t>(d.slice) * A.slice_cap;
+      }
+      const uint8_t* sb = slots + static_cast<size_t>(j) * slot_bytes;
+      const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
+      const int b0 = 32 * lane, b1 = 1024 + 32 * lane;
+      uint32_t h0 = filter_run(sb, b0);
+      uint32_t h1 = filter_run(sb, b1);
+      // positions past the step's valid range never hit
+      auto keep = [&](int base) -> uint32_t {
+        const int m = static_cast<int>(lim) - base;
+        return m >= 32 ? 0xffffffffu : (m <= 0 ? 0u : ((1u << m) - 1u));
+      };
+      h0 &= keep(b0);
+      h1 &= keep(b1);
+      verify_run(sw, d.valid, d.t, 0, h0);
+      verify_run(sw, d.valid, d.t, 1024, h1);
+      if ((flags & 2u) && lane == 0) A.slice_count[d.slice] = fill;
+      __syncwarp();
+      produce(j);  // the slot is free again
+      j = j + 1 == kRollDepth ? 0 : j + 1;
+    }
+    unsigned long long c = cands32;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(kFull, c, o);
+    if (lane == 0 && c) atomicAdd(A.counters + 1, c);
+  }
+};
+
+template <int Q, int H>
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_roll_kernel(const __grid_constant__ ScanArgs A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  extern __shared__ __align__(128) uint8_t smem[];
+  const size_t tbytes = align16(A.plan.table_bytes);
+  {
+    const uint4* src = static_cast<const uint4*>(A.table);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (size_t i = threadIdx.x; i < tbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+    __syncthreads();
+  }
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t sbytes = roll_slot_bytes(A.back);
+  uint8_t* p = smem + tbytes;
+  uint8_t* slots = p + static_cast<size_t>(warp) * kRollDepth * sbytes;
+  p += static_cast<size_t>(nw) * kRollDepth * sbytes;
+  RollDesc* desc = reinterpret_cast<RollDesc*>(p) + static_cast<size_t>(warp) * kRollDepth;
+  p += static_cast<size_t>(nw) * kRollDepth * sizeof(RollDesc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kRollDepth;
+  if ((threadIdx.x & 31) == 0) {
+    for (int j = 0; j < kRollDepth; ++j) mbar_init(bars + j, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  RollScanner<Q, H> rs(A, reinterpret_cast<const uint32_t*>(smem), slots, bars, desc, threadIdx.x & 31);
+  rs.run();
+}
+
+template <int Q, int H>
+cudaError_t launch_roll_qh(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
+  static int configured = -1;
+  if (configured != static_cast<int>(smem)) {
+    cudaError_t e = cudaFuncSetAttribute(mag_roll_kernel<Q, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = static_cast<int>(smem);
+  }
+  mag_roll_kernel<Q, H><<<grid, a.nwarps * 32, smem, stream>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <int Q>
+cudaError_t launch_roll_q(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
+  return a.plan.probes >= 3 ? launch_roll_qh<Q, 3>(a, stream, grid, smem)
+                            : launch_roll_qh<Q, 2>(a, stream, grid, smem);
+}
+
+cudaError_t launch_roll(const ScanArgs& a, cudaStream_t stream, int grid) {
+  const size_t smem = roll_smem(a.plan.roll_words, a.back, a.nwarps);
+  switch (a.plan.q) {
+    case 8: return launch_roll_q<8>(a, stream, grid, smem);
+    case 12: return launch_roll_q<12>(a, stream, grid, smem);
+    case 16: return launch_roll_q<16>(a, stream, grid, smem);
+    case 20: return launch_roll_q<20>(a, stream, grid, smem);
+    case 24: return launch_roll_q<24>(a, stream, grid, smem);
+    case 32: return launch_roll_q<32>(a, stream, grid, smem);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 // Gather: block b owns slices [b*per, (b+1)*per); its output offset is the
 // sum of all earlier slice counts (each block reduces that prefix itself —
 // at most a few tens of thousands of words from L2), then it copies its
@@ -1544,6 +1872,7 @@ LaunchShape scan_shape(const ScanArgs& a) {
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
   if (a.plan.direct) return launch_direct(a, stream, grid);
+  if (a.plan.roll) return launch_roll(a, stream, grid);
   const size_t smem = smem_layout(a.plan, a.slot_bytes, a.ring, a.nwarps).total;
   if (a.plan.smag) return launch_e<kKCodes>(a, stream, grid, smem);
   if (a.plan.gram_mode == kGramHashed) return launch_e<kKHashed>(a, stream, grid, smem);

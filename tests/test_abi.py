@@ -146,6 +146,13 @@ def test_hashed_masks_equal_restated_machine(mag, port):
         pl = e.plan()
         if pl["verify_all"] or pl["gram_mode"] != 1:
             continue
+        if pl["roll"]:
+            from pyoracle import roll_bloom
+            words = pl["table_bytes"] // 4
+            bits = e.masks(32 * words) & np.uint64(1)
+            got = np.packbits(bits.astype(np.uint8).reshape(-1, 32)[:, ::-1], axis=1).view(">u4").reshape(-1)
+            assert np.array_equal(got.astype(np.uint32), roll_bloom(pats, pl["q"], words, pl["probes"]))
+            continue
         P = port.params(variant=0 if it % 2 == 0 else 2, gram_mode=1, q=pl["q"], k=pl["k"],
                         table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
                         blocks=pl["blocks"])
@@ -206,3 +213,24 @@ def test_product_never_imports_the_oracle():
                 for bad in (r"import\s+pyoracle", r"from\s+pyoracle", r"#include\s*\S*mag_oracle",
                             r"libmagref", r"libmagoracle", r"oracle/_ref"):
                     assert not re.search(bad, src), (f, bad)
+
+
+def test_roll_bloom_equals_restatement(mag):
+    """Forced roll plans: the uploaded Bloom words equal the restated filter
+    (oracle/pyoracle.py roll_bloom) for every template q."""
+    from pyoracle import roll_bloom
+    rng = np.random.default_rng(21)
+    for m in (8, 12, 13, 16, 20, 24, 31, 32, 40):
+        pats = [(rng.integers(0, 4, m + int(rng.integers(0, 3))) + 65).astype(np.uint8).tobytes()
+                for _ in range(int(rng.integers(1, 500)))]
+        for H in (2, 3):
+            e = host_engine(mag, pats, scan_kernel="roll", probes=H)
+            pl = e.plan()
+            assert pl["roll"] == 1 and pl["variant"] == 2 and pl["probes"] == H
+            assert pl["q"] == max(c for c in (8, 12, 16, 20, 24, 32) if c <= m)
+            words = pl["table_bytes"] // 4
+            bits = e.masks(32 * words) & np.uint64(1)
+            got = np.packbits(bits.astype(np.uint8).reshape(-1, 32)[:, ::-1], axis=1).view(">u4").reshape(-1)
+            assert np.array_equal(got.astype(np.uint32), roll_bloom(pats, pl["q"], words, H))
+    with pytest.raises(mag.MagError):
+        host_engine(mag, [b"abcdefg"], scan_kernel="roll")  # m < 8: no roll plan

@@ -120,6 +120,11 @@ def test_hashed_counters_match_port(mag, ref, port):
         if pl["verify_all"]:
             assert met.candidates == met.filter_reads
             continue
+        if pl["roll"]:
+            from pyoracle import roll_candidates
+            assert met.filter_reads == max(0, text.size - pl["q"] + 1)
+            assert met.candidates == roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, pl["probes"])
+            continue
         P = port.params(variant=0 if pl["variant"] == 0 else 2, gram_mode=1, q=pl["q"], k=pl["k"],
                         table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
                         blocks=pl["blocks"])
@@ -303,3 +308,48 @@ def test_full_configs(mag, cfg):
     offs, pids = m.arrays()
     assert offs.size == want["matches"], (cfg, e.plan())
     assert match_digest(offs, pids) == want["matches_sha256"], (cfg, e.plan())
+
+
+@pytest.mark.parametrize("H", [2, 3])
+def test_roll_kernel(mag, ref, H):
+    """The dense rolling-hash scan (forced): every template q, unequal and
+    duplicate patterns, texts of every length class around the 2 KiB step
+    and 32 KiB slice, dense planted occurrences, patterns longer than the
+    staged halo (global compares); candidate counter == the restated filter."""
+    from pyoracle import roll_candidates
+    rng = np.random.default_rng(40 + H)
+    sizes = [0, 7, 8, 15, 16, 17, 2047, 2048, 2049, 2063, 32768 + 13, 100000, 300001]
+    for it, n in enumerate(sizes):
+        m = int(rng.choice([8, 9, 12, 15, 16, 20, 24, 32, 33, 48]))
+        sig = int(rng.choice([2, 4, 20, 64]))
+        text = (rng.integers(0, sig, n) + 65).astype(np.uint8)
+        r = int(rng.integers(1, 300))
+        pats = []
+        for _ in range(r):
+            L = m + int(rng.integers(0, 4))
+            if n > L and rng.random() < 0.6:
+                s0 = int(rng.integers(0, n - L + 1))
+                pats.append(text[s0:s0 + L].tobytes())
+            else:
+                pats.append((rng.integers(0, sig, L) + 65).astype(np.uint8).tobytes())
+        if it % 3 == 0 and n > 400:
+            pats.append(text[n - 300:n].tobytes())   # longer than the halo, ends at n
+            pats.append(pats[0])                     # duplicate pattern id
+        text = text.copy()
+        for _ in range(n // 50):                      # dense plants
+            p = pats[int(rng.integers(0, len(pats)))]
+            if len(p) < n:
+                s0 = int(rng.integers(0, n - len(p) + 1))
+                text[s0:s0 + len(p)] = np.frombuffer(p, dtype=np.uint8)
+        e = mag.Engine(pats, scan_kernel="roll", probes=H)
+        pl = e.plan()
+        assert pl["roll"] == 1
+        got, met = gpu_pairs(e, text)
+        assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
+        assert met.candidates == roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, H), (n, m)
+        # misaligned device text takes the aligned-copy path
+        if n > 64:
+            import torch
+            d = torch.from_numpy(text).cuda()
+            pd = e.prepare_device(d.data_ptr() + 5, n - 5, keep=d)
+            assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[5:], pats))
