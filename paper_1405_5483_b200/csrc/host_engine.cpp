@@ -141,6 +141,7 @@ struct mag_engine {
   uint32_t* d_l2map = nullptr;
   uint32_t* d_bucket_start = nullptr;
   uint32_t* d_entries = nullptr;
+  uint32_t* d_vtab = nullptr;
   uint8_t* d_pat_bytes = nullptr;
   uint64_t* d_pat_off = nullptr;
   uint32_t* d_pat_len = nullptr;
@@ -160,6 +161,7 @@ struct mag_engine {
       cudaFree(d_l2map);
       cudaFree(d_bucket_start);
       cudaFree(d_entries);
+      cudaFree(d_vtab);
       cudaFree(d_pat_bytes);
       cudaFree(d_pat_off);
       cudaFree(d_pat_len);
@@ -312,6 +314,8 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.bucket_start = e->d_bucket_start;
     a.l2map = e->d_l2map;
     a.bucket_entries = reinterpret_cast<const uint2*>(e->d_entries);
+    a.vtab = reinterpret_cast<const uint4*>(e->d_vtab);
+    a.vmask = e->ptab.vmask;
     a.pat_bytes = e->d_pat_bytes;
     a.pat_off = e->d_pat_off;
     a.pat_len = e->d_pat_len;
@@ -432,6 +436,7 @@ mag_status upload_engine(mag_engine* e) {
   MAG_CUDA(upload(e->ptab.l2map, &e->d_l2map));
   MAG_CUDA(upload(e->ptab.bucket_start, &e->d_bucket_start));
   MAG_CUDA(upload(e->ptab.entries, &e->d_entries));
+  MAG_CUDA(upload(e->ptab.vtab, &e->d_vtab));
   MAG_CUDA(upload(e->pd.bytes, &e->d_pat_bytes));
   MAG_CUDA(upload(e->pd.off, &e->d_pat_off));
   MAG_CUDA(upload(e->pd.len, &e->d_pat_len));

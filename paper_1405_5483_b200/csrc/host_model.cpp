@@ -542,7 +542,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         (rq.q == 0 || rq.q == 16) &&
         rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0) {
       const unsigned q = 16;
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16;
       ScanPlan z{};
       const size_t fixed = direct_smem(z, warps) + 1024;
       const size_t room = rq.smem_limit > fixed ? rq.smem_limit - fixed : 0;
@@ -708,7 +708,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.pf_bits = pf;
   } else {
     sp.table_in_smem = sp.verify_all ? 0 : 1;
-    if (sp.direct) P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+    if (sp.direct) P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16;
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
@@ -864,6 +864,28 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
     for (const Ent& e : ents) {
       const uint32_t b = screen_bit(e.key, sp.l2_bits);
       pt->l2map[b >> 5] |= 1u << (b & 31);
+    }
+  }
+  // roll plans: open addressing by the start key, linear probing; patterns
+  // inserted in id order, so equal keys are met in id order along a probe run
+  pt->vtab.assign(8 * 16, 0);
+  pt->vmask = 0;
+  if (sp.roll) {
+    size_t slots = 16;
+    while (slots < 2 * r) slots <<= 1;
+    pt->vmask = static_cast<uint32_t>(slots - 1);
+    pt->vtab.assign(8 * slots, 0);
+    for (size_t i = 0; i < slots; ++i) pt->vtab[8 * i + 1] = 0xffffffffu;
+    for (size_t i = 0; i < r; ++i) {
+      const uint32_t key = key_bytes(pd.pattern(i), sp.key_len);
+      size_t s = key & pt->vmask;
+      while (pt->vtab[8 * s + 1] != 0xffffffffu) s = (s + 1) & pt->vmask;
+      uint32_t* e = &pt->vtab[8 * s];
+      e[0] = key;
+      e[1] = static_cast<uint32_t>(i);
+      e[2] = pd.len[i];
+      e[3] = static_cast<uint32_t>(pd.off[i] / 16);
+      std::memcpy(e + 4, pd.pattern(i), 16);  // patterns are zero padded to 16 bytes
     }
   }
   // buckets by low key bits, stable within a bucket

@@ -111,6 +111,10 @@ struct PatternTable {
   std::vector<uint32_t> l2map;
   std::vector<uint32_t> bucket_start;
   std::vector<uint32_t> entries;  // interleaved key, pid
+  // roll plans: open-addressing verification table, 8 words per slot
+  // {key, pid (0xffffffff = empty), len, pattern offset / 16, first 16 bytes}
+  std::vector<uint32_t> vtab;
+  uint32_t vmask = 0;
 };
 void build_pattern_table(const Plan& plan, const PatternData& pd, PatternTable* pt);
 

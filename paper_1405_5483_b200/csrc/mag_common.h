@@ -197,10 +197,12 @@ struct SmemLayout {
 // Direct (q = 16) kernel: resident table, per-warp probe queue, and a ring
 // of kDirectDepth 1 KiB step buffers (+ mbarriers) per warp.
 constexpr int kDirectDepth = 4;
+constexpr int kDirectMaxWarps = 24;  // direct kernel: up to 768 threads (3-deep rings past 16 warps)
+MAG_HD int direct_depth(uint32_t nwarps) { return nwarps > 16 ? 3 : kDirectDepth; }
 constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lane
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
-         size_t(nwarps) * kDirectDepth * (kDirectStep * 16) + size_t(nwarps) * kDirectDepth * (16 + 8) + 64;
+         size_t(nwarps) * direct_depth(nwarps) * (kDirectStep * 16 + 16 + 8) + 64;
 }
 
 // Roll kernel: Bloom words, per-warp ring of kRollDepth slots of

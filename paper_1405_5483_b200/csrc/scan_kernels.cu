@@ -1088,7 +1088,7 @@ struct __align__(16) DirectDesc {
   uint32_t t, slice, lim_flags, pad;
 };
 
-template <int H>
+template <int H, int DEPTH>
 struct DirectScanner {
   const ScanArgs& A;
   const int lane;
@@ -1106,18 +1106,24 @@ struct DirectScanner {
   // producer cursor (warp-uniform)
   uint32_t p_t, p_left;
   bool p_done;
+  uint64_t pol;  // L2 evict-first policy of the text stream (created once)
 
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint4* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
-        pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false) {
+        pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
     for (int i = 0; i < kPer; ++i) pend_w[i] = pend_b[i] = pend_k[i] = 0;
     pend_pos = 0;
   }
 
   // Claim the next step and stage it into ring slot j (TMA bulk copy,
-  // completion on bars[j]); an invalid descriptor marks the end.
-  __device__ __forceinline__ void produce(int j) {
+  // completion on bars[j]); an invalid descriptor marks the end.  `dep` is
+  // computed from every value this warp last loaded from slot j and feeds
+  // the TMA byte count, so those shared-memory loads have returned before
+  // the async proxy overwrites the slot (an empty asm operand would not
+  // make ptxas wait on the loads' scoreboard: that race lost the last
+  // quarter of a step's samples under load).
+  __device__ __forceinline__ void produce(int j, uint32_t dep = 0) {
     uint32_t slice = 0;
     bool first = false;
     while (!p_done && p_left == 0) {
@@ -1146,12 +1152,14 @@ struct DirectScanner {
       } else {
         const uint32_t lim = p_left < kStep ? p_left : kStep;
         d.t = p_t;
-        d.slice = first ? slice : desc[j == 0 ? kDirectDepth - 1 : j - 1].slice;
+        d.slice = first ? slice : desc[j == 0 ? DEPTH - 1 : j - 1].slice;
         d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= kStep ? 2u : 0u)) << 8);
         d.pad = 0;
-        mbar_arrive_expect_tx(bars + j, 16u * lim);
-        tma_load_1d_stream(slots + j * kDirectStep, A.text + 16ull * p_t, 16u * lim, bars + j,
-                           policy_evict_first());
+        // (dep & A.zero) == 0, but only at run time: the byte count, hence the
+        // TMA issue, data-depends on every word loaded from the slot
+        const uint32_t bytes = 16u * lim + (dep & A.zero);
+        mbar_arrive_expect_tx(bars + j, bytes);
+        tma_load_1d_stream(slots + j * kDirectStep, A.text + 16ull * p_t, bytes, bars + j, pol);
       }
       desc[j] = d;
     }
@@ -1191,14 +1199,11 @@ struct DirectScanner {
   // Filter the lane's kPer samples of a step; a filter hit issues its L2
   // screen load now and is resolved one step later (resolve()), so the L2
   // round trip overlaps the next step's filtering instead of stalling.
-  __device__ __forceinline__ void filter(const uint4 (&v)[kPer], uint32_t lim) {
+  __device__ __forceinline__ void filter(const uint4 (&v)[kPer], const uint32_t (&h)[kPer], uint32_t lim) {
     const uint32_t lb = A.plan.l2_bits;
     const bool count_only = A.plan.diag & 8;  // diagnostics: no screen / verification
-    uint32_t h[kPer];
     bool hit[kPer];
     // all lookups first (independent shared-memory loads in flight together)
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) h[i] = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
 #pragma unroll
     for (int i = 0; i < kPer; ++i) hit[i] = admits(h[i]);
 #pragma unroll
@@ -1216,7 +1221,7 @@ struct DirectScanner {
       pend_b[i] = sb & 31u;
       // the screen word is only consumed by resolve() one step later
       uint32_t w = 0;
-      if (hit[i] && !count_only) w = lb ? __ldg(A.l2map + (sb >> 5)) : 1u;
+      if (hit[i] && !count_only) w = (lb && !(A.plan.diag & 128)) ? __ldg(A.l2map + (sb >> 5)) : ~0u;
       pend_w[i] = w;
     }
   }
@@ -1233,7 +1238,7 @@ struct DirectScanner {
     for (int i = 0; i < kPer; ++i) pend_w[i] = 0;
   }
 
-  __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer]) {
+  __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
     const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
     if (flags & 1u) {
       fill = 0;
@@ -1244,7 +1249,8 @@ struct DirectScanner {
       resolve();  // the previous step of this slice
     }
     pend_pos = 16u * (d.t - pbase_t) + 16u * lane;
-    filter(v, lim);
+    filter(v, h, lim);
+    if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
     if (flags & 2u) {
       resolve();
       if (pqn) flush();
@@ -1254,7 +1260,7 @@ struct DirectScanner {
 
   __device__ void run() {
 #pragma unroll 1
-    for (int j = 0; j < kDirectDepth; ++j) produce(j);
+    for (int j = 0; j < DEPTH; ++j) produce(j);
     __syncwarp();
     uint32_t phase = 0;  // bit j: parity of slot j's next completion
     int j = 0;
@@ -1265,17 +1271,22 @@ struct DirectScanner {
       mbar_wait(bars + j, (phase >> j) & 1u);
       phase ^= 1u << j;
       uint4 v[kPer];
+      uint32_t h[kPer];
 #pragma unroll
       for (int i = 0; i < kPer; ++i) v[i] = slots[j * kDirectStep + 32 * i + lane];
-      // the slot's shared-memory reads must have completed before the TMA
-      // refill below overwrites it: wait for the loaded values here
+      // the gram hashes consume every loaded word; their xor gates the TMA
+      // refill of this slot (see produce)
+      uint32_t dep = 0;
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) asm volatile("" ::"r"(v[i].x));
+      for (int i = 0; i < kPer; ++i) {
+        h[i] = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
+        dep ^= h[i];
+      }
       __syncwarp();
-      produce(j);  // refill the slot just read
+      produce(j, dep);  // refill the slot just read
       __syncwarp();
-      process(d, v);
-      j = j + 1 == kDirectDepth ? 0 : j + 1;
+      process(d, v, h);
+      j = j + 1 == DEPTH ? 0 : j + 1;
     }
     unsigned long long c = cands32;
 #pragma unroll
@@ -1284,8 +1295,8 @@ struct DirectScanner {
   }
 };
 
-template <int H>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
+template <int H, int DEPTH, int NT>
+__global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
   // let the dependent gather grid launch early (it waits for our completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1300,32 +1311,38 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_direct_kernel(const __g
   uint8_t* p = smem + tbytes;
   uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kProbeCap;
   p += align16(size_t(nw) * kProbeCap * 8);
-  uint4* slots = reinterpret_cast<uint4*>(p) + static_cast<size_t>(warp) * kDirectDepth * kDirectStep;
-  p += size_t(nw) * kDirectDepth * kDirectStep * 16;
-  DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * kDirectDepth;
-  p += size_t(nw) * kDirectDepth * sizeof(DirectDesc);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kDirectDepth;
+  uint4* slots = reinterpret_cast<uint4*>(p) + static_cast<size_t>(warp) * DEPTH * kDirectStep;
+  p += size_t(nw) * DEPTH * kDirectStep * 16;
+  DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
+  p += size_t(nw) * DEPTH * sizeof(DirectDesc);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
   if ((threadIdx.x & 31) == 0) {
-    for (int j = 0; j < kDirectDepth; ++j) mbar_init(bars + j, 1);
+    for (int j = 0; j < DEPTH; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  DirectScanner<H> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
+  DirectScanner<H, DEPTH> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
   ds.run();
+}
+
+template <int H, int DEPTH, int NT>
+cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
+  static int configured = -1;
+  if (configured != static_cast<int>(smem)) {
+    cudaError_t e = cudaFuncSetAttribute(mag_direct_kernel<H, DEPTH, NT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = static_cast<int>(smem);
+  }
+  mag_direct_kernel<H, DEPTH, NT><<<grid, a.nwarps * 32, smem, stream>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 template <int H>
 cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  static int configured = -1;
-  if (configured != static_cast<int>(smem)) {
-    cudaError_t e = cudaFuncSetAttribute(mag_direct_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = static_cast<int>(smem);
-  }
-  mag_direct_kernel<H><<<grid, a.nwarps * 32, smem, stream>>>(a);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32>(a, stream, grid, smem);
+  return launch_direct_hd<H, kDirectDepth, 512>(a, stream, grid, smem);
 }
 
 cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
@@ -1384,11 +1401,12 @@ struct RollScanner {
   unsigned long long p_t, p_end;
   uint32_t p_slice;
   bool p_done, p_first;
+  uint64_t pol;
 
   __device__ RollScanner(const ScanArgs& a, const uint32_t* bl, uint8_t* sl, uint64_t* b, RollDesc* d, int l)
       : A(a), lane(l), bloom(bl), slots(sl), bars(b), desc(d), slot_bytes(roll_slot_bytes(a.back)),
         bq(roll_pow(Q)), fill(0), cands32(0), out(nullptr), p_t(0), p_end(0), p_slice(0), p_done(false),
-        p_first(false) {}
+        p_first(false), pol(policy_evict_first()) {}
 
   // Claim (if needed) and stage the next step into slot j.
   __device__ __forceinline__ void produce(int j) {
@@ -1432,7 +1450,7 @@ struct RollScanner {
       d.lim_flags = lim | ((4u | (p_first ? 1u : 0u) | (p_t + lim >= p_end ? 2u : 0u)) << 16);
       fence_proxy_async();
       mbar_arrive_expect_tx(bars + j, bulk);
-      if (bulk) tma_load_1d_stream(dst, A.text + p_t, bulk, bars + j, policy_evict_first());
+      if (bulk) tma_load_1d_stream(dst, A.text + p_t, bulk, bars + j, pol);
     }
     __syncwarp();
     p_t += lim;
@@ -1476,16 +1494,21 @@ struct RollScanner {
     return hits;
   }
 
-  // Start key (first key_len bytes) at slot offset pr.
-  __device__ __forceinline__ uint32_t key_at(const uint32_t* sw, uint32_t pr) const {
-    const uint32_t wi = pr >> 2, sh = (pr & 3u) << 3, v = A.plan.key_len;
+  // The 16 text bytes at slot offset pr (four little-endian words).
+  static __device__ __forceinline__ uint4 text16(const uint32_t* sw, uint32_t pr) {
+    const uint32_t wi = pr >> 2, sh = (pr & 3u) << 3;
     uint32_t x[5];
 #pragma unroll
     for (int k = 0; k < 5; ++k) x[k] = sw[wi + k];
-    return key_words(__funnelshift_r(x[0], x[1], sh) & key_word_mask(v, 0),
-                     __funnelshift_r(x[1], x[2], sh) & key_word_mask(v, 1),
-                     __funnelshift_r(x[2], x[3], sh) & key_word_mask(v, 2),
-                     __funnelshift_r(x[3], x[4], sh) & key_word_mask(v, 3));
+    return make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh),
+                      __funnelshift_r(x[2], x[3], sh), __funnelshift_r(x[3], x[4], sh));
+  }
+
+  // Start key: the first key_len bytes (mag_common.h key_words).
+  __device__ __forceinline__ uint32_t key_of(const uint4& t) const {
+    const uint32_t v = A.plan.key_len;
+    return key_words(t.x & key_word_mask(v, 0), t.y & key_word_mask(v, 1), t.z & key_word_mask(v, 2),
+                     t.w & key_word_mask(v, 3));
   }
 
   // Pattern pid (len bytes) against the staged text at slot offset pr.
@@ -1510,19 +1533,26 @@ struct RollScanner {
     return true;
   }
 
-  // Matches at slot offset pr: counted (first pid kept), or written from dst[idx].
+  // Matches at slot offset pr (text bytes t, start key): one L2 round trip
+  // per verification slot — {key, pid, len, off} and the pattern's first 16
+  // bytes sit in the same 32-byte sector; longer patterns finish against
+  // the pattern bytes.  Counted (first pid kept), or written from dst[idx].
   __device__ uint32_t probe(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
-                            uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first) const {
-    const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
-    const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
-    uint32_t c = 0;
-    for (uint32_t e = lo; e < hi; ++e) {
-      const uint2 ent = __ldg(A.bucket_entries + e);
-      if (ent.x != key) continue;
-      const uint32_t len = __ldg(A.pat_len + ent.y);
-      if (a + len > A.n || !equal_slot(sw, valid, a, pr, ent.y, len)) continue;
-      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, ent.y);
-      if (c == 0 && first) *first = ent.y;
+                            const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first) const {
+    uint32_t s = key & A.vmask, c = 0;
+    for (;;) {
+      const uint4 h = __ldg(A.vtab + 2 * s);
+      const uint4 b = __ldg(A.vtab + 2 * s + 1);
+      if (h.y == 0xffffffffu) break;
+      s = (s + 1) & A.vmask;
+      if (h.x != key || a + h.z > A.n) continue;
+      const uint32_t len = h.z;
+      const uint32_t d = ((t.x ^ b.x) & key_word_mask(len, 0)) | ((t.y ^ b.y) & key_word_mask(len, 1)) |
+                         ((t.z ^ b.z) & key_word_mask(len, 2)) | ((t.w ^ b.w) & key_word_mask(len, 3));
+      if (d) continue;
+      if (len > 16 && !equal_slot(sw, valid, a, pr, h.y, len)) continue;
+      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h.y);
+      if (c == 0 && first) *first = h.y;
       ++c;
     }
     return c;
@@ -1548,12 +1578,14 @@ struct RollScanner {
       const uint32_t hm = __shfl_sync(kFull, hits, o);
       const uint32_t eo = __shfl_sync(kFull, excl, o);
       uint32_t c = 0, pid0 = 0, key = 0, pr = 0;
+      uint4 tx = make_uint4(0, 0, 0, 0);
       unsigned long long a = 0;
       if (live) {
         pr = static_cast<uint32_t>(run_base + 32 * o + static_cast<int>(__fns(hm, 0, static_cast<int>(rank - eo) + 1)));
         a = t + pr;
-        key = key_at(sw, pr);
-        c = probe(sw, valid, a, pr, key, nullptr, 0, &pid0);
+        tx = text16(sw, pr);
+        key = key_of(tx);
+        c = probe(sw, valid, a, pr, tx, key, nullptr, 0, &pid0);
       }
       if (!__any_sync(kFull, c != 0)) continue;
       const uint32_t ex = warp_excl_scan(c, lane);
@@ -1561,7 +1593,7 @@ struct RollScanner {
       if (c == 1) {
         if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(a, pid0);
       } else if (c > 1) {
-        probe(sw, valid, a, pr, key, out, fill + ex, nullptr);
+        probe(sw, valid, a, pr, tx, key, out, fill + ex, nullptr);
       }
       fill += tot;
     }

@@ -29,6 +29,9 @@ struct ScanArgs {
   const uint64_t* pat_off;
   const uint32_t* pat_len;
   const uint8_t* map;           // 256-byte alphabet map (exact grams)
+  const uint4* vtab;            // roll: verification slots (2 x uint4 each), vmask + 1 of them
+  uint32_t vmask;
+  uint32_t zero;                // always 0; opaque to the compiler (orders slot reads before TMA refills)
   uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping, n verify-all
   uint64_t slice_samples;       // multiple of chunk_samples
   uint32_t chunk_samples;       // samples per chunk (iterations * advance)
