@@ -346,7 +346,7 @@ def _roll_slots(h: np.ndarray, words: int, probes: int):
     with np.errstate(over="ignore"):
         g = h.astype(np.uint32) * np.uint32(ROLL_MIX)
     w = ((g.astype(np.uint64) * np.uint64(words)) >> np.uint64(32)).astype(np.int64)
-    bits = [((g >> np.uint32(5 * i)) & np.uint32(31)).astype(np.uint32) for i in range(probes)]
+    bits = [(np.uint32(31) - ((g >> np.uint32(5 * i)) & np.uint32(31))).astype(np.uint32) for i in range(probes)]
     return w, bits
 
 

@@ -798,7 +798,7 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
     for (size_t i = 0; i < pd.r; ++i) {
       const uint32_t g = roll_hash_bytes(pd.pattern(i), sp.q) * kRollMix;
       const uint32_t wi = roll_word(g, sp.roll_words);
-      for (unsigned j = 0; j < sp.probes; ++j) w[wi] |= 1u << ((g >> (5 * j)) & 31u);
+      for (unsigned j = 0; j < sp.probes; ++j) w[wi] |= 1u << (31u - ((g >> (5 * j)) & 31u));
     }
     return;
   }
@@ -872,7 +872,7 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   pt->vmask = 0;
   if (sp.roll) {
     size_t slots = 16;
-    while (slots < 2 * r) slots <<= 1;
+    while (slots < 4 * r) slots <<= 1;  // load factor <= 1/4
     pt->vmask = static_cast<uint32_t>(slots - 1);
     pt->vtab.assign(8 * slots, 0);
     for (size_t i = 0; i < slots; ++i) pt->vtab[8 * i + 1] = 0xffffffffu;

@@ -72,7 +72,7 @@ MAG_HD uint32_t bloom_bit(uint64_t g, unsigned i) { return static_cast<uint32_t>
 // Rolling q-gram hash of the dense (roll) scan: H(p) = sum_{j<q} t[p+j] *
 // B^(q-1-j) mod 2^32, so H(p+1) = H(p)*B + t[p+q] - t[p]*B^q (two IMADs per
 // position).  Its filter is a blocked Bloom filter of 32-bit words: word
-// umulhi(g, words), bits (g >> 5i) & 31 for i < probes, g = H * kRollMix.
+// umulhi(g, words), bits 31 - ((g >> 5i) & 31) for i < probes, g = H * kRollMix.
 constexpr uint32_t kRollB = 0x9E3779B1u;
 constexpr uint32_t kRollMix = 0x2C1B3C6Du;
 constexpr int kRollMaxProbes = 4;

@@ -1238,9 +1238,11 @@ struct DirectScanner {
     for (int i = 0; i < kPer; ++i) pend_w[i] = 0;
   }
 
-  __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
-    const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
-    if (flags & 1u) {
+  // Step prologue (independent of the step's data: runs while its
+  // shared-memory loads are in flight): a new slice resets the output
+  // cursor, otherwise the previous step's screen loads are resolved.
+  __device__ __forceinline__ void begin(const DirectDesc& d) {
+    if ((d.lim_flags >> 8) & 1u) {
       fill = 0;
       pqn = 0;
       pbase_t = d.t;
@@ -1248,6 +1250,10 @@ struct DirectScanner {
     } else {
       resolve();  // the previous step of this slice
     }
+  }
+
+  __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
+    const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
     pend_pos = 16u * (d.t - pbase_t) + 16u * lane;
     filter(v, h, lim);
     if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
@@ -1274,13 +1280,14 @@ struct DirectScanner {
       uint32_t h[kPer];
 #pragma unroll
       for (int i = 0; i < kPer; ++i) v[i] = slots[j * kDirectStep + 32 * i + lane];
-      // the gram hashes consume every loaded word; their xor gates the TMA
-      // refill of this slot (see produce)
+      begin(d);
+      // one word of every 16-byte load gates the TMA refill of this slot (a
+      // vector load returns all its words together; see produce)
       uint32_t dep = 0;
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         h[i] = hash_gram_words(v[i].x, v[i].y, v[i].z, v[i].w);
-        dep ^= h[i];
+        dep ^= v[i].x;
       }
       __syncwarp();
       produce(j, dep);  // refill the slot just read
@@ -1334,6 +1341,7 @@ cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, s
     if (e != cudaSuccess) return e;
     configured = static_cast<int>(smem);
   }
+  (void)cudaGetLastError();
   mag_direct_kernel<H, DEPTH, NT><<<grid, a.nwarps * 32, smem, stream>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -1461,16 +1469,22 @@ struct RollScanner {
     return __byte_perm(w[k >> 2], 0u, 0x4440u | static_cast<uint32_t>(k & 3));
   }
 
+  // Bloom probe bits sit at 31 - ((g >> 5i) & 31), so rotl(word, g >> 5i)
+  // (funnel shift, wrap mode: the count is taken mod 32) brings each to bit
+  // 31; their AND's bit 31 is the verdict.
   __device__ __forceinline__ uint32_t test(uint32_t h) const {
     const uint32_t g = h * kRollMix;
     const uint32_t wd = bloom[roll_word(g, A.plan.roll_words)];
-    uint32_t r = __funnelshift_r(wd, wd, g);
+    uint32_t r = __funnelshift_l(wd, wd, g);
 #pragma unroll
-    for (int i = 1; i < H; ++i) r &= __funnelshift_r(wd, wd, g >> (5 * i));
-    return r & 1u;
+    for (int i = 1; i < H; ++i) r &= __funnelshift_l(wd, wd, g >> (5 * i));
+    return r;  // verdict in bit 31
   }
 
-  // Bloom hits of the lane's run starting at slot offset `base` (32 positions).
+  // Bloom hits of the lane's run starting at slot offset `base` (32
+  // positions; bit p = position base + p).  Prefix form of the rolling hash:
+  // P(i+1) = P(i)*B + t[i], H(p) = P(p+Q) - P(p)*B^Q — one byte extraction
+  // and two IMADs per position.
   __device__ __forceinline__ uint32_t filter_run(const uint8_t* sb, int base) const {
     uint32_t w[kW];
     const uint4* src = reinterpret_cast<const uint4*>(sb + base);
@@ -1482,16 +1496,14 @@ struct RollScanner {
       w[4 * v + 2] = x.z;
       w[4 * v + 3] = x.w;
     }
-    uint32_t h = 0;
+    uint32_t P[kRun + Q];
+    P[0] = 0;
 #pragma unroll
-    for (int k = 0; k < Q; ++k) h = h * kRollB + byte_at(w, k);
-    uint32_t hits = test(h);
+    for (int i = 0; i + 1 < kRun + Q; ++i) P[i + 1] = P[i] * kRollB + byte_at(w, i);
+    uint32_t hits = 0;
 #pragma unroll
-    for (int i = 1; i < kRun; ++i) {
-      h = h * kRollB + (byte_at(w, i + Q - 1) - byte_at(w, i - 1) * bq);
-      hits |= test(h) << i;
-    }
-    return hits;
+    for (int p = 0; p < kRun; ++p) hits = __funnelshift_l(test(P[p + Q] - P[p] * bq), hits, 1);
+    return __brev(hits);
   }
 
   // The 16 text bytes at slot offset pr (four little-endian words).
@@ -1537,65 +1549,113 @@ struct RollScanner {
   // per verification slot — {key, pid, len, off} and the pattern's first 16
   // bytes sit in the same 32-byte sector; longer patterns finish against
   // the pattern bytes.  Counted (first pid kept), or written from dst[idx].
+  // One verification slot against the candidate: 1 = match.
+  __device__ __forceinline__ bool slot_match(const uint32_t* sw, uint32_t valid, unsigned long long a,
+                                             uint32_t pr, const uint4& t, uint32_t key, const uint4& h,
+                                             const uint4& b) const {
+    if (h.x != key || a + h.z > A.n) return false;
+    const uint32_t len = h.z;
+    const uint32_t d = ((t.x ^ b.x) & key_word_mask(len, 0)) | ((t.y ^ b.y) & key_word_mask(len, 1)) |
+                       ((t.z ^ b.z) & key_word_mask(len, 2)) | ((t.w ^ b.w) & key_word_mask(len, 3));
+    if (d) return false;
+    return len <= 16 || equal_slot(sw, valid, a, pr, h.y, len);
+  }
+
+  // Linear-probe run from the key's home slot; slots are consumed in pairs
+  // (h0,b0 = home, h1,b1 = next: both loaded in one round trip), so with a
+  // load factor <= 1/4 nearly every run ends inside the first pair.
   __device__ uint32_t probe(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
-                            const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first) const {
+                            const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first,
+                            uint4 h0, uint4 b0, uint4 h1, uint4 b1) const {
     uint32_t s = key & A.vmask, c = 0;
     for (;;) {
-      const uint4 h = __ldg(A.vtab + 2 * s);
-      const uint4 b = __ldg(A.vtab + 2 * s + 1);
-      if (h.y == 0xffffffffu) break;
-      s = (s + 1) & A.vmask;
-      if (h.x != key || a + h.z > A.n) continue;
-      const uint32_t len = h.z;
-      const uint32_t d = ((t.x ^ b.x) & key_word_mask(len, 0)) | ((t.y ^ b.y) & key_word_mask(len, 1)) |
-                         ((t.z ^ b.z) & key_word_mask(len, 2)) | ((t.w ^ b.w) & key_word_mask(len, 3));
-      if (d) continue;
-      if (len > 16 && !equal_slot(sw, valid, a, pr, h.y, len)) continue;
-      if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h.y);
-      if (c == 0 && first) *first = h.y;
-      ++c;
+      if (h0.y == 0xffffffffu) break;
+      if (slot_match(sw, valid, a, pr, t, key, h0, b0)) {
+        if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h0.y);
+        if (c == 0 && first) *first = h0.y;
+        ++c;
+      }
+      if (h1.y == 0xffffffffu) break;
+      if (slot_match(sw, valid, a, pr, t, key, h1, b1)) {
+        if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h1.y);
+        if (c == 0 && first) *first = h1.y;
+        ++c;
+      }
+      s = (s + 2) & A.vmask;
+      h0 = __ldg(A.vtab + 2 * s);
+      b0 = __ldg(A.vtab + 2 * s + 1);
+      const uint32_t s1 = (s + 1) & A.vmask;
+      h1 = __ldg(A.vtab + 2 * s1);
+      b1 = __ldg(A.vtab + 2 * s1 + 1);
     }
     return c;
   }
 
-  // Expand and verify the hits of one run (lane masks, text order).
-  __device__ void verify_run(const uint32_t* sw, uint32_t valid, unsigned long long t, int run_base,
-                             uint32_t hits) {
-    const uint32_t cnt = __popc(hits);
-    const uint32_t excl = warp_excl_scan(cnt, lane);
-    const uint32_t total = __shfl_sync(kFull, excl + cnt, 31);
-    cands32 += cnt;
+  // Expand and verify a step's hits in text order: run 0 (positions
+  // [32 l, 32 l + 32) of lane l) before run 1 ([1024 + 32 l, ...)).  Two
+  // candidates per lane per batch, so both verification-slot loads (one L2
+  // round trip each) are in flight together.
+  static constexpr int kVK = 2;
+  __device__ void verify_step(const uint32_t* sw, uint32_t valid, unsigned long long t, uint32_t h0,
+                              uint32_t h1) {
+    const uint32_t c0 = __popc(h0), c1 = __popc(h1);
+    const uint32_t e0 = warp_excl_scan(c0, lane), e1 = warp_excl_scan(c1, lane);
+    const uint32_t t0 = __shfl_sync(kFull, e0 + c0, 31), t1 = __shfl_sync(kFull, e1 + c1, 31);
+    const uint32_t total = t0 + t1;
+    cands32 += c0 + c1;
     if (A.plan.diag & 8) return;
-    for (uint32_t r0 = 0; r0 < total; r0 += 32) {
-      const uint32_t rank = r0 + lane;
-      const bool live = rank < total;
-      int o = 0;
+    const uint32_t packed = e0 | (e1 << 16);
+    for (uint32_t base = 0; base < total; base += 32 * kVK) {
+      uint32_t pr[kVK], key[kVK], c[kVK], pid0[kVK];
+      uint4 tx[kVK], hq[kVK], bq[kVK], hn[kVK], bn[kVK];
+      bool live[kVK];
 #pragma unroll
-      for (int step = 16; step; step >>= 1) {
-        const uint32_t e = __shfl_sync(kFull, excl, o + step);
-        if (e <= rank) o += step;
+      for (int k = 0; k < kVK; ++k) {
+        const uint32_t rank = base + 32 * k + lane;
+        live[k] = rank < total;
+        const bool r1 = rank >= t0;
+        const uint32_t rr = r1 ? rank - t0 : rank;
+        const uint32_t sh = r1 ? 16u : 0u;
+        int o = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const uint32_t e = (__shfl_sync(kFull, packed, o + step) >> sh) & 0xffffu;
+          if (e <= rr) o += step;
+        }
+        const uint32_t m0 = __shfl_sync(kFull, h0, o), m1 = __shfl_sync(kFull, h1, o);
+        const uint32_t eo = (__shfl_sync(kFull, packed, o) >> sh) & 0xffffu;
+        pr[k] = (r1 ? 1024u : 0u) + 32u * static_cast<uint32_t>(o) +
+                static_cast<uint32_t>(__fns(r1 ? m1 : m0, 0, static_cast<int>(rr - eo) + 1));
+        if (!live[k]) pr[k] = 0;
+        tx[k] = text16(sw, pr[k]);
+        key[k] = key_of(tx[k]);
+        const uint32_t slot = key[k] & A.vmask, slot1 = (slot + 1) & A.vmask;
+        const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
+        hq[k] = live[k] ? __ldg(A.vtab + 2 * slot) : empty;
+        bq[k] = live[k] ? __ldg(A.vtab + 2 * slot + 1) : empty;
+        hn[k] = live[k] ? __ldg(A.vtab + 2 * slot1) : empty;
+        bn[k] = live[k] ? __ldg(A.vtab + 2 * slot1 + 1) : empty;
       }
-      const uint32_t hm = __shfl_sync(kFull, hits, o);
-      const uint32_t eo = __shfl_sync(kFull, excl, o);
-      uint32_t c = 0, pid0 = 0, key = 0, pr = 0;
-      uint4 tx = make_uint4(0, 0, 0, 0);
-      unsigned long long a = 0;
-      if (live) {
-        pr = static_cast<uint32_t>(run_base + 32 * o + static_cast<int>(__fns(hm, 0, static_cast<int>(rank - eo) + 1)));
-        a = t + pr;
-        tx = text16(sw, pr);
-        key = key_of(tx);
-        c = probe(sw, valid, a, pr, tx, key, nullptr, 0, &pid0);
+#pragma unroll
+      for (int k = 0; k < kVK; ++k) {
+        pid0[k] = 0;
+        c[k] = probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], nullptr, 0, &pid0[k], hq[k], bq[k], hn[k],
+                     bn[k]);
       }
-      if (!__any_sync(kFull, c != 0)) continue;
-      const uint32_t ex = warp_excl_scan(c, lane);
-      const uint32_t tot = __shfl_sync(kFull, ex + c, 31);
-      if (c == 1) {
-        if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(a, pid0);
-      } else if (c > 1) {
-        probe(sw, valid, a, pr, tx, key, out, fill + ex, nullptr);
+#pragma unroll
+      for (int k = 0; k < kVK; ++k) {
+        if (!__any_sync(kFull, c[k] != 0)) continue;
+        const uint32_t ex = warp_excl_scan(c[k], lane);
+        const uint32_t tot = __shfl_sync(kFull, ex + c[k], 31);
+        if (c[k] == 1) {
+          if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], pid0[k]);
+        } else if (c[k] > 1) {
+          const uint32_t slot = key[k] & A.vmask, slot1 = (slot + 1) & A.vmask;
+          probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], out, fill + ex, nullptr, __ldg(A.vtab + 2 * slot),
+                __ldg(A.vtab + 2 * slot + 1), __ldg(A.vtab + 2 * slot1), __ldg(A.vtab + 2 * slot1 + 1));
+        }
+        fill += tot;
       }
-      fill += tot;
     }
   }
 
@@ -1627,8 +1687,7 @@ struct RollScanner {
       };
       h0 &= keep(b0);
       h1 &= keep(b1);
-      verify_run(sw, d.valid, d.t, 0, h0);
-      verify_run(sw, d.valid, d.t, 1024, h1);
+      verify_step(sw, d.valid, d.t, h0, h1);
       if ((flags & 2u) && lane == 0) A.slice_count[d.slice] = fill;
       __syncwarp();
       produce(j);  // the slot is free again
@@ -1678,6 +1737,7 @@ cudaError_t launch_roll_qh(const ScanArgs& a, cudaStream_t stream, int grid, siz
     if (e != cudaSuccess) return e;
     configured = static_cast<int>(smem);
   }
+  (void)cudaGetLastError();
   mag_roll_kernel<Q, H><<<grid, a.nwarps * 32, smem, stream>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -1836,6 +1896,7 @@ cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) 
     if (e != cudaSuccess) return e;
     configured_smem = static_cast<int>(smem);
   }
+  (void)cudaGetLastError();  // a stale error of another runtime user (e.g. torch) is not ours
   k<<<grid, a.nwarps * 32, smem, st>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -1925,6 +1986,7 @@ cudaError_t launch_compact(const ScanArgs& a, uint64_t* out, uint64_t out_cap, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  (void)cudaGetLastError();
   cudaError_t e = cudaLaunchKernelEx(&cfg, mag_compact_kernel, a, out, out_cap);
   if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -1938,6 +2000,7 @@ cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,
   const int threads = 256;
   uint64_t blocks = (nq + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  (void)cudaGetLastError();
   mag_encode_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(plan, text, nq, map,
                                                                            codes);
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -344,7 +344,10 @@ def test_roll_kernel(mag, ref, H):
         e = mag.Engine(pats, scan_kernel="roll", probes=H)
         pl = e.plan()
         assert pl["roll"] == 1
-        got, met = gpu_pairs(e, text)
+        try:
+            got, met = gpu_pairs(e, text)
+        except mag.MagError as ex:
+            raise AssertionError(f"n={n} m={m} sig={sig} r={len(pats)} plan={pl}: {ex}")
         assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
         assert met.candidates == roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, H), (n, m)
         # misaligned device text takes the aligned-copy path
