@@ -342,11 +342,16 @@ def roll_hashes(text, q: int) -> np.ndarray:
     return h
 
 
+ROLL_PROBE_MUL = {1: 0x85EBCA77, 2: 0xC2B2AE3D}
+
+
 def _roll_slots(h: np.ndarray, words: int, probes: int):
     with np.errstate(over="ignore"):
         g = h.astype(np.uint32) * np.uint32(ROLL_MIX)
     w = ((g.astype(np.uint64) * np.uint64(words)) >> np.uint64(32)).astype(np.int64)
-    bits = [(np.uint32(31) - ((g >> np.uint32(5 * i)) & np.uint32(31))).astype(np.uint32) for i in range(probes)]
+    shifts = [g] + [((h.astype(np.uint64) * np.uint64(ROLL_PROBE_MUL[i])) >> np.uint64(32)).astype(np.uint32)
+                    for i in range(1, probes)]
+    bits = [(np.uint32(31) - (s & np.uint32(31))).astype(np.uint32) for s in shifts]
     return w, bits
 
 

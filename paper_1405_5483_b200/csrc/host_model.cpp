@@ -245,10 +245,18 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostChunk = 4800,  // per staged chunk (loader + bookkeeping), thread-instr
                  kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
                  kCostPf = 15,       // shared-memory prefilter test
-                 kCostDirectHit = 6,  // direct kernel: a filter hit issues one L2 screen load
-                 kCostRollPos = 17,   // roll kernel: roll + one Bloom word per position (2 probes)
-                 kCostRollProbe = 2,  // each further Bloom probe
-                 kCostRollCand = 90;  // expansion + start key + bucket walk of a Bloom hit
+                 kCostDirectHit = 120,  // direct kernel: a filter hit issues one L2 screen load
+                 kCostRollPos = 24,   // roll kernel: roll + one Bloom word per position
+                 kCostRollProbe = 2.5,  // each Bloom probe
+                 kCostRollWarm = 2,   // prefix warm-up (q bytes per 32-position run)
+                 kCostRollCand = 800;  // expansion + start key + verification-slot round trip of a hit
+// Round-1 B200 calibration: the staged kernel's measured cost per
+// text byte is ~4x the instruction model above plus a fixed ~15 (ring
+// bookkeeping, queue drains, verification latency); the direct kernel's
+// per-sample filter work scales the same way, and one direct-kernel filter
+// hit (L2 screen load + deferred resolve) costs ~120.
+constexpr double kStagedScale = 4, kStagedFloor = 15;
+double staged_scale(double model) { return kStagedScale * model + kStagedFloor; }
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
 // when `keys` keys of v bytes are drawn over the pattern alphabet.
@@ -446,10 +454,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       for (uint32_t chunk : kChunks) {
         if (rq.tile_bytes > 0 && chunk != kChunks[0]) break;
         if (pf_bytes(pf) > room_for(1, 1, 1, 1, chunk)) continue;
-        const double cost = kCostVerifyAll + kCostChunk / chunk +
+        const double cost = staged_scale(kCostVerifyAll + kCostChunk / chunk +
                             (pf ? prefilter_fp(keys, pf) : 1.0) * kCostProbe +
                             key_hits(keys, sigma_obs, static_cast<unsigned>(std::min<size_t>(m, 16))) *
-                                kCostCompare;
+                                kCostCompare);
         if (cost < best.cost) {
           best.cost = cost;
           best.pf = pf;
@@ -517,6 +525,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                                  fp * (kCostScreen + 0.01 * kCostProbe) + hits * kCostCompare);
                 else       // start keys: one probe per verified start
                   cost += cpb * kCostCand + pm * (kCostStart + fp * kCostProbe + hits * kCostCompare);
+                cost = staged_scale(cost);
                 if (cost < best.cost * 0.999) {
                   best.cost = cost;
                   best.q = q;
@@ -563,7 +572,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         const double cpb = p / q;
         // a filter hit only issues its L2 screen load (resolved a step later);
         // ~1/128 of them, plus the true starts, reach a bucket walk
-        const double cost = (kCostSample + H * kCostProbeBit) / q +
+        const double cost = kStagedScale * (kCostSample + 2 * H * kCostProbeBit) / q +
                             cpb * (kCostDirectHit + 0.008 * (kCostCand + kCostProbe + hits * kCostCompare));
         if (cost < best.cost * 0.999) {
           best.cost = cost;
@@ -603,13 +612,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           rq.smem_limit > fixed ? static_cast<uint32_t>((rq.smem_limit - fixed) / 16 * 4) : 0;
       const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
       const double exact = universe > 1e15 ? 0.0 : std::min(1.0, keys / universe);
-      for (unsigned H = 2; q && words >= 1024 && H <= 3; ++H) {
+      for (unsigned H = 1; q && words >= 1024 && H <= 3; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
         const double bits = 32.0 * words;
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * keys / bits);
         const double fp = std::min(1.0, 1.4 * std::pow(fill, static_cast<double>(H)));  // blocked penalty
         const double cpb = exact + (1.0 - exact) * fp;
-        const double cost = kCostRollPos + (H - 2) * kCostRollProbe + cpb * kCostRollCand;
+        const double cost = kCostRollPos + H * kCostRollProbe + kCostRollWarm * q / 32.0 + cpb * kCostRollCand;
         if (cost < best.cost * 0.999) {
           best = Cand{};
           best.cost = cost;
@@ -796,9 +805,10 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
     table->assign(sp.table_bytes, 0);
     uint32_t* w = reinterpret_cast<uint32_t*>(table->data());
     for (size_t i = 0; i < pd.r; ++i) {
-      const uint32_t g = roll_hash_bytes(pd.pattern(i), sp.q) * kRollMix;
-      const uint32_t wi = roll_word(g, sp.roll_words);
-      for (unsigned j = 0; j < sp.probes; ++j) w[wi] |= 1u << (31u - ((g >> (5 * j)) & 31u));
+      const uint32_t h = roll_hash_bytes(pd.pattern(i), sp.q);
+      const uint32_t wi = roll_word(h * kRollMix, sp.roll_words);
+      for (unsigned j = 0; j < sp.probes; ++j)
+        w[wi] |= 1u << (31u - (roll_probe_shift(h, static_cast<int>(j)) & 31u));
     }
     return;
   }

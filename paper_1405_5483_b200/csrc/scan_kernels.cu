@@ -1398,6 +1398,7 @@ struct RollScanner {
   const ScanArgs& A;
   const int lane;
   const uint32_t* bloom;
+  uint32_t bloom_s;         // shared-window address of the Bloom words
   uint8_t* slots;
   uint64_t* bars;
   RollDesc* desc;
@@ -1412,7 +1413,8 @@ struct RollScanner {
   uint64_t pol;
 
   __device__ RollScanner(const ScanArgs& a, const uint32_t* bl, uint8_t* sl, uint64_t* b, RollDesc* d, int l)
-      : A(a), lane(l), bloom(bl), slots(sl), bars(b), desc(d), slot_bytes(roll_slot_bytes(a.back)),
+      : A(a), lane(l), bloom(bl), bloom_s(smem_addr(bl)), slots(sl), bars(b), desc(d),
+        slot_bytes(roll_slot_bytes(a.back)),
         bq(roll_pow(Q)), fill(0), cands32(0), out(nullptr), p_t(0), p_end(0), p_slice(0), p_done(false),
         p_first(false), pol(policy_evict_first()) {}
 
@@ -1469,15 +1471,20 @@ struct RollScanner {
     return __byte_perm(w[k >> 2], 0u, 0x4440u | static_cast<uint32_t>(k & 3));
   }
 
-  // Bloom probe bits sit at 31 - ((g >> 5i) & 31), so rotl(word, g >> 5i)
-  // (funnel shift, wrap mode: the count is taken mod 32) brings each to bit
-  // 31; their AND's bit 31 is the verdict.
+  // Bloom probe bits sit at 31 - (s_i & 31) (mag_common.h roll_probe_shift),
+  // so rotl(word, s_i) (funnel shift, wrap mode: the count is taken mod 32)
+  // brings each to bit 31; their AND's bit 31 is the verdict.  s_0 = g and
+  // s_i = umulhi(h, C_i): the extra probes cost fma-pipe IMAD.HIs, not
+  // alu-pipe shifts.
   __device__ __forceinline__ uint32_t test(uint32_t h) const {
     const uint32_t g = h * kRollMix;
-    const uint32_t wd = bloom[roll_word(g, A.plan.roll_words)];
+    // word address by IMAD (fma pipe; the alu pipe is the busier one)
+    uint32_t addr, wd;
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(roll_word(g, A.plan.roll_words)), "r"(bloom_s));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(wd) : "r"(addr));
     uint32_t r = __funnelshift_l(wd, wd, g);
 #pragma unroll
-    for (int i = 1; i < H; ++i) r &= __funnelshift_l(wd, wd, g >> (5 * i));
+    for (int i = 1; i < H; ++i) r &= __funnelshift_l(wd, wd, __umulhi(h, roll_probe_mul(i)));
     return r;  // verdict in bit 31
   }
 
@@ -1745,8 +1752,9 @@ cudaError_t launch_roll_qh(const ScanArgs& a, cudaStream_t stream, int grid, siz
 
 template <int Q>
 cudaError_t launch_roll_q(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  return a.plan.probes >= 3 ? launch_roll_qh<Q, 3>(a, stream, grid, smem)
-                            : launch_roll_qh<Q, 2>(a, stream, grid, smem);
+  if (a.plan.probes >= 3) return launch_roll_qh<Q, 3>(a, stream, grid, smem);
+  if (a.plan.probes == 2) return launch_roll_qh<Q, 2>(a, stream, grid, smem);
+  return launch_roll_qh<Q, 1>(a, stream, grid, smem);
 }
 
 cudaError_t launch_roll(const ScanArgs& a, cudaStream_t stream, int grid) {
