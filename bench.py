@@ -155,6 +155,64 @@ def cpu_reference(workload, budget_s=12.0, threads=None):
     return size / dt / 1e9, threads, sample, kind
 
 
+def config_sweep(cfgs, local, steps=10, warmup=3):
+    """Every other BASELINE.json config, device-resident: step and scan-kernel
+    GB/s, fraction of HBM, the plan, and whether the full-size match set's
+    count + sha256 equal the reference AC's (tests/golden/full_digests.json)."""
+    import hashlib
+    import numpy as np
+    import torch
+    import paper_1405_5483_b200 as mag
+    from paper_1405_5483_b200 import workloads
+    peak, _ = peaks()
+    with open(os.path.join(ROOT, "tests", "golden", "full_digests.json")) as f:
+        digests = json.load(f)
+    out = {}
+    for c in cfgs:
+        w = workloads.generate(c, 1.0)
+        eng = mag.Engine(w.patterns, device=local)
+        d = torch.from_numpy(w.text).to(f"cuda:{local}")
+        prep = eng.prepare_device(d.data_ptr(), w.text.size, keep=d)
+        m = eng.search_prepared(prep)
+        offs, pids = m.arrays()
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(offs, dtype="<u8").tobytes())
+        h.update(np.ascontiguousarray(pids, dtype="<u4").tobytes())
+        want = digests.get(str(c), {})
+        ok = int(offs.size) == want.get("matches") and h.hexdigest() == want.get("matches_sha256")
+        m.close()
+        st = torch.cuda.Stream()
+        for _ in range(warmup):
+            eng.search_prepared_async(prep, st.cuda_stream).close()
+        # inputs below L2 size (cfg1, 16 MiB) are re-read from L2: flush it
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}") if w.text.size < (256 << 20) else None
+        torch.cuda.synchronize()
+        mag.scan_timer(True)
+        ms = 0.0
+        for _ in range(steps):
+            if flush is not None:
+                flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            eng.search_prepared_async(prep, st.cuda_stream).close()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+        kms, kl = mag.scan_timer_read()
+        mag.scan_timer(False)
+        n = int(w.text.size)
+        step_gbs = n / (ms / steps * 1e-3) / 1e9
+        kern_gbs = n / (kms / max(kl, 1) * 1e-3) / 1e9
+        pl = eng.plan()
+        out[f"cfg{c}"] = {"workload": w.name, "n": n, "r": len(w.patterns), "GB/s": step_gbs, "kernel_GB/s": kern_gbs,
+                          "frac_of_hbm": kern_gbs / peak, "matches": int(offs.size), "bit_exact_vs_reference": bool(ok),
+                          "l2": "flushed between steps" if flush is not None else "input larger than L2",
+                          "plan": {k: pl[k] for k in ("variant", "q", "k", "m_prime", "probes", "direct", "roll")}}
+        del d, prep, eng, flush
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -166,6 +224,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--check", action="store_true", help="also verify the match set against oracle/_ref AC")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the per-config sweep of the other BASELINE.json configs")
     args = ap.parse_args()
     rank, world, local = dist_env()
     from paper_1405_5483_b200 import workloads
@@ -224,6 +284,16 @@ def main():
     n_matches = len(first)
     metrics = first.metrics()
     checked = None
+    digest_ok = None
+    if world == 1 and args.scale == 1.0:
+        import hashlib
+        with open(os.path.join(ROOT, "tests", "golden", "full_digests.json")) as f:
+            want = json.load(f).get(str(args.config), {})
+        offs, pids = first.arrays()
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(offs, dtype="<u8").tobytes())
+        h.update(np.ascontiguousarray(pids, dtype="<u4").tobytes())
+        digest_ok = int(offs.size) == want.get("matches") and h.hexdigest() == want.get("matches_sha256")
     if args.check:
         from pyoracle import Ref
         want = Ref().ac(w.text, w.patterns, threads=os.cpu_count())
@@ -303,6 +373,9 @@ def main():
                 traffic = json.load(f).get(f"cfg{args.config}")
         except Exception:
             traffic = None
+    sweep = None
+    if not args.headline_only and world == 1:
+        sweep = config_sweep([c for c in (1, 2, 3, 4, 5) if c != args.config], local)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         gbs, cores, sample, kind = cpu_reference(w)
@@ -319,7 +392,8 @@ def main():
                                                  "entry_bits", "verify_all", "prefilter_bits", "tile_bytes",
                                                  "warps", "stages", "smem_bytes")},
                    "matches": n_matches, "job_matches": total_matches, "filter_reads": metrics.filter_reads,
-                   "candidates": metrics.candidates, "checked_vs_reference_ac": checked},
+                   "candidates": metrics.candidates, "checked_vs_reference_ac": checked,
+                   "bit_exact_vs_reference_digest": digest_ok},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": n},
@@ -328,6 +402,7 @@ def main():
                 "api": "mag_search (pinned host text) + clip + rank-ordered gather"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
+        "configs": sweep,
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -608,11 +608,14 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       const uint32_t halo = static_cast<uint32_t>(
           align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
       const size_t fixed = roll_smem(0, halo, warps) + 1024;
-      const uint32_t words =
-          rq.smem_limit > fixed ? static_cast<uint32_t>((rq.smem_limit - fixed) / 16 * 4) : 0;
+      // Bloom words: what shared memory leaves, but no more than ~128 bits per
+      // pattern (every CTA loads the table: small sets keep it small)
+      const size_t room_words = rq.smem_limit > fixed ? (rq.smem_limit - fixed) / 16 * 4 : 0;
+      const uint32_t words = static_cast<uint32_t>(
+          std::min<size_t>(room_words, std::max<size_t>(1024, (4 * pd.r + 3) / 4 * 4)));
       const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
       const double exact = universe > 1e15 ? 0.0 : std::min(1.0, keys / universe);
-      for (unsigned H = 1; q && words >= 1024 && H <= 3; ++H) {
+      for (unsigned H = 1; q && room_words >= 1024 && H <= 3; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
         const double bits = 32.0 * words;
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * keys / bits);

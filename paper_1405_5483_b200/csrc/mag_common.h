@@ -214,7 +214,7 @@ MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
 
 // Roll kernel: Bloom words, per-warp ring of kRollDepth slots of
 // kRollStep text bytes + halo (+ mbarriers and step descriptors).
-constexpr int kRollDepth = 3;
+constexpr int kRollDepth = 2;
 constexpr int kRollStep = 2048;   // positions per step: 2 runs of 32 per lane
 MAG_HD uint32_t roll_slot_bytes(uint32_t halo) { return static_cast<uint32_t>(align16(kRollStep + halo)); }
 MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
