@@ -247,7 +247,8 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostPf = 15,       // shared-memory prefilter test
                  kCostDirectHit = 120,  // direct kernel: a filter hit issues one L2 screen load
                  kCostRollPos = 24,   // roll kernel: roll + one Bloom word per position
-                 kCostRollProbe = 2.5,  // each Bloom probe
+                 kCostRollProbe = 1.5,  // each Bloom probe
+                 kCostRollBatch = 6,  // a verification batch (expansion, keys, slot loads) per 64 bytes of lane work
                  kCostRollWarm = 2,   // prefix warm-up (q bytes per 32-position run)
                  kCostRollCand = 800;  // expansion + start key + verification-slot round trip of a hit
 // Round-1 B200 calibration: the staged kernel's measured cost per
@@ -608,11 +609,11 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       const uint32_t halo = static_cast<uint32_t>(
           align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
       const size_t fixed = roll_smem(0, halo, warps) + 1024;
-      // Bloom words: what shared memory leaves, but no more than ~128 bits per
+      // Bloom words: what shared memory leaves, but no more than ~2 Kibit per
       // pattern (every CTA loads the table: small sets keep it small)
       const size_t room_words = rq.smem_limit > fixed ? (rq.smem_limit - fixed) / 16 * 4 : 0;
       const uint32_t words = static_cast<uint32_t>(
-          std::min<size_t>(room_words, std::max<size_t>(1024, (4 * pd.r + 3) / 4 * 4)));
+          std::min<size_t>(room_words, std::max<size_t>(4096, (64 * pd.r + 3) / 4 * 4)));
       const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
       const double exact = universe > 1e15 ? 0.0 : std::min(1.0, keys / universe);
       for (unsigned H = 1; q && room_words >= 1024 && H <= 3; ++H) {
@@ -621,7 +622,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * keys / bits);
         const double fp = std::min(1.0, 1.4 * std::pow(fill, static_cast<double>(H)));  // blocked penalty
         const double cpb = exact + (1.0 - exact) * fp;
-        const double cost = kCostRollPos + H * kCostRollProbe + kCostRollWarm * q / 32.0 + cpb * kCostRollCand;
+        // a step (2048 positions) with any hit pays one verification batch
+        const double batch = 1.0 - std::exp(-cpb * kRollStep);
+        const double cost = kCostRollPos + H * kCostRollProbe + kCostRollWarm * q / 32.0 + cpb * kCostRollCand +
+                            batch * kCostRollBatch;
         if (cost < best.cost * 0.999) {
           best = Cand{};
           best.cost = cost;

@@ -1685,8 +1685,14 @@ struct RollScanner {
       const uint8_t* sb = slots + static_cast<size_t>(j) * slot_bytes;
       const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
       const int b0 = 32 * lane, b1 = 1024 + 32 * lane;
-      uint32_t h0 = filter_run(sb, b0);
-      uint32_t h1 = filter_run(sb, b1);
+      // one copy of the (large, fully unrolled) run body: instruction-cache
+      // footprint matters with 16 warps at different points of the step
+      uint32_t h0 = 0, h1 = 0;
+#pragma unroll 1
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t x = filter_run(sb, r ? b1 : b0);
+        if (r) h1 = x; else h0 = x;
+      }
       // positions past the step's valid range never hit
       auto keep = [&](int base) -> uint32_t {
         const int m = static_cast<int>(lim) - base;
