@@ -119,13 +119,13 @@ MAG_HD uint32_t key_bytes(const uint8_t* p, unsigned v) {
   return key_words(x[0], x[1], x[2], x[3]);
 }
 
-// L2 screen bit of a window key: re-mixed so it is independent of the
-// filter table slot (which uses the top bits of the same gram hash).
+// L2 screen bit of a window key: its low l2_bits bits (one LOP).  For the
+// direct kernel's key (the gram hash, whose top bits index the filter
+// table) a filter hit fixes only the screen index's top 32 - 19 bits to an
+// admitted key's, and ~r*q / 2^19 keys share those, so the screen stays as
+// selective as an independent bitmap of the same density.
 MAG_HD uint32_t screen_bit(uint32_t key, unsigned l2_bits) {
-  uint32_t x = key * 0x7FEB352Du;
-  x ^= x >> 15;
-  x *= 0x846CA68Bu;
-  return x >> (32 - l2_bits);
+  return l2_bits >= 32 ? key : (key & ((1u << l2_bits) - 1u));
 }
 
 // Byte masks of the v-byte key per word.
