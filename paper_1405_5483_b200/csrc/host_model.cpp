@@ -547,25 +547,28 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         }
       }
     }
-    // direct q = 16 stream kernel: no staging, the table takes the smem
-    if ((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 31 &&
-        (rq.q == 0 || rq.q == 16) &&
-        rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0) {
-      const unsigned q = 16;
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16;
+    // direct stream kernel (q = 16 or 8 byte aligned samples): no gram
+    // staging, the table takes the smem; an occurrence (m >= 2q - 1) always
+    // covers one whole aligned sample, at one of q shifts
+    for (unsigned q : {16u, 8u}) {
+      if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
+            (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0))
+        continue;
+      const uint32_t warps = q == 8 ? 16 : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16);
       ScanPlan z{};
+      z.q = q;
       const size_t fixed = direct_smem(z, warps) + 1024;
       const size_t room = rq.smem_limit > fixed ? rq.smem_limit - fixed : 0;
       const uint32_t blocks = static_cast<uint32_t>(std::min<size_t>(room / 8, 1u << 22));
-      const double universe = std::pow(static_cast<double>(sigma_obs), 16.0);
+      const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
       const double adm = keys * q;
       const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
       const double exact = universe > 1e15 ? 0.0 : distinct / universe;
-      const double hits = key_hits(adm, sigma_obs, static_cast<unsigned>(std::min<size_t>(16, m - q + 1)));
+      const double hits = key_hits(adm, sigma_obs, q);
       // single probe: largest power-of-two table that fits
       unsigned tb1 = 6;
       while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room) ++tb1;
-      for (unsigned H = 1; H <= kMaxProbes && blocks > 0; ++H) {
+      for (unsigned H = 1; H <= (q == 8 ? 4u : kMaxProbes) && blocks > 0; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
         const double bits = H == 1 ? std::ldexp(1.0, static_cast<int>(tb1)) : 64.0 * blocks;
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / bits);
@@ -724,11 +727,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.pf_bits = pf;
   } else {
     sp.table_in_smem = sp.verify_all ? 0 : 1;
-    if (sp.direct) P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16;
+    if (sp.direct)
+      P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, sp.q == 8 ? 16u : kDirectMaxWarps) : 16;
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
-  sp.key_gram = sp.direct && sp.wkey_len == 16;
+  if (sp.direct) sp.wkey_len = sp.q;  // the window key is the aligned sample itself
+  sp.key_gram = sp.direct;
   sp.l2_bits = 0;
   if (sp.window_key) {  // ~128 bits per key: ~0.8% of screened keys walk a bucket
     unsigned lb = 16;
@@ -856,7 +861,7 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
     ents.reserve(r * sp.q);
     for (int s = static_cast<int>(sp.q) - 1; s >= 0; --s)
       for (size_t i = 0; i < r; ++i)
-        ents.push_back({sp.key_gram ? hash_gram_bytes(pd.pattern(i) + s, 16)
+        ents.push_back({sp.key_gram ? hash_gram_bytes(pd.pattern(i) + s, sp.q)
                                     : key_bytes(pd.pattern(i) + s, sp.wkey_len),
                         static_cast<uint32_t>(i) | (static_cast<uint32_t>(s) << kPidBits)});
   } else {

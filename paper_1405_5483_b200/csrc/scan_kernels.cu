@@ -1088,13 +1088,14 @@ struct __align__(16) DirectDesc {
   uint32_t t, slice, lim_flags, pad;
 };
 
-template <int H, int DEPTH>
+template <int H, int DEPTH, int W>
 struct DirectScanner {
+  static_assert(W == 8 || W == 16, "sample width");
   const ScanArgs& A;
   const int lane;
   const void* table;
   uint2* pq;
-  uint4* slots;       // [kDirectDepth][kDirectStep] staged samples
+  uint8_t* slots;     // [DEPTH][kDirectStep * W] staged samples
   uint64_t* bars;     // [kDirectDepth]
   DirectDesc* desc;   // [kDirectDepth]
   uint32_t pqn, fill, cands32;
@@ -1108,7 +1109,7 @@ struct DirectScanner {
   bool p_done;
   uint64_t pol;  // L2 evict-first policy of the text stream (created once)
 
-  __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint4* sl, uint64_t* b, DirectDesc* dsc,
+  __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
         pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
@@ -1157,9 +1158,10 @@ struct DirectScanner {
         d.pad = 0;
         // (dep & A.zero) == 0, but only at run time: the byte count, hence the
         // TMA issue, data-depends on every word loaded from the slot
-        const uint32_t bytes = 16u * lim + (dep & A.zero);
+        const uint32_t bytes = W * lim + (dep & A.zero);
         mbar_arrive_expect_tx(bars + j, bytes);
-        tma_load_1d_stream(slots + j * kDirectStep, A.text + 16ull * p_t, bytes, bars + j, pol);
+        tma_load_1d_stream(slots + static_cast<size_t>(j) * kDirectStep * W, A.text + static_cast<uint64_t>(W) * p_t,
+                           bytes, bars + j, pol);
       }
       desc[j] = d;
     }
@@ -1182,7 +1184,7 @@ struct DirectScanner {
 
   __device__ __forceinline__ void flush() {
     if (!(A.plan.diag & 16))
-      fill = flush_queue(A, pq, pqn, 16ull * pbase_t, out, fill, lane, true);
+      fill = flush_queue(A, pq, pqn, static_cast<unsigned long long>(W) * pbase_t, out, fill, lane, true);
     pqn = 0;
   }
 
@@ -1232,7 +1234,7 @@ struct DirectScanner {
     for (int i = 0; i < kPer; ++i) surv |= ((pend_w[i] >> pend_b[i]) & 1u) << i;
     if (__any_sync(kFull, surv != 0)) {
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 512u * i);
+      for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 32u * W * i);
     }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) pend_w[i] = 0;
@@ -1254,7 +1256,7 @@ struct DirectScanner {
 
   __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
     const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
-    pend_pos = 16u * (d.t - pbase_t) + 16u * lane;
+    pend_pos = W * (d.t - pbase_t) + W * lane;
     filter(v, h, lim);
     if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
     if (flags & 2u) {
@@ -1279,7 +1281,14 @@ struct DirectScanner {
       uint4 v[kPer];
       uint32_t h[kPer];
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) v[i] = slots[j * kDirectStep + 32 * i + lane];
+      for (int i = 0; i < kPer; ++i) {
+        if constexpr (W == 16) {
+          v[i] = reinterpret_cast<const uint4*>(slots + static_cast<size_t>(j) * kDirectStep * W)[32 * i + lane];
+        } else {
+          const uint2 x = reinterpret_cast<const uint2*>(slots + static_cast<size_t>(j) * kDirectStep * W)[32 * i + lane];
+          v[i] = make_uint4(x.x, x.y, 0u, 0u);
+        }
+      }
       begin(d);
       // one word of every 16-byte load gates the TMA refill of this slot (a
       // vector load returns all its words together; see produce)
@@ -1302,7 +1311,7 @@ struct DirectScanner {
   }
 };
 
-template <int H, int DEPTH, int NT>
+template <int H, int DEPTH, int NT, int W>
 __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
   // let the dependent gather grid launch early (it waits for our completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1318,8 +1327,8 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
   uint8_t* p = smem + tbytes;
   uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kProbeCap;
   p += align16(size_t(nw) * kProbeCap * 8);
-  uint4* slots = reinterpret_cast<uint4*>(p) + static_cast<size_t>(warp) * DEPTH * kDirectStep;
-  p += size_t(nw) * DEPTH * kDirectStep * 16;
+  uint8_t* slots = p + static_cast<size_t>(warp) * DEPTH * kDirectStep * W;
+  p += size_t(nw) * DEPTH * kDirectStep * W;
   DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
   p += size_t(nw) * DEPTH * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
@@ -1328,29 +1337,33 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  DirectScanner<H, DEPTH> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
+  DirectScanner<H, DEPTH, W> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
   ds.run();
 }
 
-template <int H, int DEPTH, int NT>
+template <int H, int DEPTH, int NT, int W>
 cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
   static int configured = -1;
   if (configured != static_cast<int>(smem)) {
-    cudaError_t e = cudaFuncSetAttribute(mag_direct_kernel<H, DEPTH, NT>,
+    cudaError_t e = cudaFuncSetAttribute(mag_direct_kernel<H, DEPTH, NT, W>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = static_cast<int>(smem);
   }
   (void)cudaGetLastError();
-  mag_direct_kernel<H, DEPTH, NT><<<grid, a.nwarps * 32, smem, stream>>>(a);
+  mag_direct_kernel<H, DEPTH, NT, W><<<grid, a.nwarps * 32, smem, stream>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 template <int H>
 cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32>(a, stream, grid, smem);
-  return launch_direct_hd<H, kDirectDepth, 512>(a, stream, grid, smem);
+  if (a.plan.q == 8) {  // 8-byte samples (m >= 15)
+    if constexpr (H <= 4) return launch_direct_hd<H, kDirectDepth, 512, 8>(a, stream, grid, smem);
+    return cudaErrorInvalidValue;
+  }
+  if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32, 16>(a, stream, grid, smem);
+  return launch_direct_hd<H, kDirectDepth, 512, 16>(a, stream, grid, smem);
 }
 
 cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
