@@ -559,15 +559,17 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       z.q = q;
       const size_t fixed = direct_smem(z, warps) + 1024;
       const size_t room = rq.smem_limit > fixed ? rq.smem_limit - fixed : 0;
-      const uint32_t blocks = static_cast<uint32_t>(std::min<size_t>(room / 8, 1u << 22));
-      const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
+      // tables of at most ~64 bits per admitted gram (every CTA loads its copy)
       const double adm = keys * q;
+      const size_t cap_bits = std::max<size_t>(size_t(1) << 14, static_cast<size_t>(adm * 64));
+      const uint32_t blocks = static_cast<uint32_t>(std::min<size_t>({room / 8, size_t(1) << 22, cap_bits / 64}));
+      const double universe = std::pow(static_cast<double>(sigma_obs), static_cast<double>(q));
       const double distinct = universe > 1e15 ? adm : universe * (1.0 - std::exp(-adm / universe));
       const double exact = universe > 1e15 ? 0.0 : distinct / universe;
       const double hits = key_hits(adm, sigma_obs, q);
       // single probe: largest power-of-two table that fits
       unsigned tb1 = 6;
-      while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room) ++tb1;
+      while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room && (size_t(1) << tb1) < cap_bits) ++tb1;
       for (unsigned H = 1; H <= (q == 8 ? 4u : kMaxProbes) && blocks > 0; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
         const double bits = H == 1 ? std::ldexp(1.0, static_cast<int>(tb1)) : 64.0 * blocks;

@@ -1158,10 +1158,16 @@ struct DirectScanner {
         d.pad = 0;
         // (dep & A.zero) == 0, but only at run time: the byte count, hence the
         // TMA issue, data-depends on every word loaded from the slot
-        const uint32_t bytes = W * lim + (dep & A.zero);
+        // bulk copies move whole 16-byte units: an odd 8-byte sample count
+        // (the text's last step) leaves one sample for a plain load
+        const uint32_t total = W * lim, bulk = total & ~15u;
+        uint8_t* dst = slots + static_cast<size_t>(j) * kDirectStep * W;
+        const uint8_t* src = A.text + static_cast<uint64_t>(W) * p_t;
+        if (total != bulk)
+          *reinterpret_cast<uint2*>(dst + bulk) = __ldg(reinterpret_cast<const uint2*>(src + bulk));
+        const uint32_t bytes = bulk + (dep & A.zero);
         mbar_arrive_expect_tx(bars + j, bytes);
-        tma_load_1d_stream(slots + static_cast<size_t>(j) * kDirectStep * W, A.text + static_cast<uint64_t>(W) * p_t,
-                           bytes, bars + j, pol);
+        if (bulk) tma_load_1d_stream(dst, src, bytes, bars + j, pol);
       }
       desc[j] = d;
     }

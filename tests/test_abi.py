@@ -234,3 +234,16 @@ def test_roll_bloom_equals_restatement(mag):
             assert np.array_equal(got.astype(np.uint32), roll_bloom(pats, pl["q"], words, H))
     with pytest.raises(mag.MagError):
         host_engine(mag, [b"abcdefg"], scan_kernel="roll")  # m < 8: no roll plan
+
+
+def test_planner_picks_the_calibrated_kernel_per_config(mag):
+    """The five BASELINE shapes (reduced text; plans depend on the pattern
+    set only): aligned 16-byte samples for m = 32, 8-byte samples for m = 16,
+    the dense rolling-hash scan for r = 100k, m = 12 (DESIGN.md kernels)."""
+    from paper_1405_5483_b200 import workloads
+    want = {1: ("direct", 8), 2: ("direct", 16), 3: ("direct", 8), 4: ("direct", 16), 5: ("roll", 12)}
+    for cfg, (kernel, q) in want.items():
+        w = workloads.generate(cfg, 1 / 256)
+        pl = host_engine(mag, w.patterns).plan()
+        assert pl[kernel] == 1 and pl["q"] == q, (cfg, pl)
+        assert pl["smem_bytes"] <= 232448
