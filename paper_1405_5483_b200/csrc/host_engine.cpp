@@ -74,7 +74,7 @@ struct Workspace {
   cudaEvent_t done = nullptr;
   int device = 0;
   // geometry of the last enqueued search
-  uint64_t num_slices = 0, slice_cap = 0;
+  uint64_t num_slices = 0, slice_cap = 0, slice_samples = 0;
 
   ~Workspace() {
     cudaSetDevice(device);
@@ -230,14 +230,27 @@ constexpr size_t kCounters = 8;
 constexpr size_t kCtrlWords = kCounters + kMaxLaunch;
 
 struct SearchGeometry {
-  uint64_t samples, num_slices, slice_cap;
+  uint64_t samples, slice_samples, num_slices, slice_cap;
 };
+
+// Slices are the warps' work items: the plan's size, but small texts get
+// smaller slices (whole kernel steps) so that every warp of the grid has
+// about four of them.
+uint64_t slice_samples_for(const mag_engine* e, uint64_t samples) {
+  const Plan& P = e->plan;
+  const uint64_t unit = P.sp.roll ? kRollStep : (P.sp.direct ? kDirectStep : P.chunk_samples);
+  const uint64_t warps = static_cast<uint64_t>(e->sm_count) * P.nwarps * 4;
+  uint64_t want = (samples + warps - 1) / warps;
+  want = (want + unit - 1) / unit * unit;
+  return std::max<uint64_t>(unit, std::min<uint64_t>(P.slice_samples, want));
+}
 
 SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) {
   const Plan& P = e->plan;
   SearchGeometry g;
   g.samples = filter_reads(P, n);
-  g.num_slices = (g.samples + P.slice_samples - 1) / P.slice_samples;
+  g.slice_samples = slice_samples_for(e, g.samples);
+  g.num_slices = (g.samples + g.slice_samples - 1) / g.slice_samples;
   if (cap_override) {
     g.slice_cap = cap_override;
   } else {
@@ -247,9 +260,9 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
       dens = e->slice_density;
     }
     // until a search has been seen: 1 match per 128 text bytes of a slice
-    const double bytes = static_cast<double>(P.slice_samples) *
+    const double bytes = static_cast<double>(g.slice_samples) *
                          (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
-    const double guess = std::max(dens * static_cast<double>(P.slice_samples) * 1.25, bytes / 128);
+    const double guess = std::max(dens * static_cast<double>(g.slice_samples) * 1.25, bytes / 128);
     g.slice_cap = std::max<uint64_t>(64, static_cast<uint64_t>(guess) + 32);
   }
   return g;
@@ -299,6 +312,7 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   if (s != MAG_OK) return s;
   w->num_slices = g.num_slices;
   w->slice_cap = g.slice_cap;
+  w->slice_samples = g.slice_samples;
   unsigned long long* counters = w->ctrl + w->parity * kCtrlWords;
   unsigned long long* next_ctrl = w->ctrl + (w->parity ^ 1u) * kCtrlWords;
   w->parity ^= 1u;
@@ -321,7 +335,7 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.pat_len = e->d_pat_len;
     a.map = e->d_map;
     a.samples = g.samples;
-    a.slice_samples = P.slice_samples;
+    a.slice_samples = g.slice_samples;
     a.chunk_samples = P.chunk_samples;
     a.back = P.back;
     a.slot_bytes = P.slot_bytes;
@@ -383,7 +397,7 @@ mag_status materialize(mag_matches* m) {
     maxc = w->h_ctr[3];
   }
   {
-    const double dens = static_cast<double>(maxc) / static_cast<double>(e->plan.slice_samples);
+    const double dens = static_cast<double>(maxc) / static_cast<double>(std::max<uint64_t>(1, w->slice_samples));
     std::lock_guard<std::mutex> lk(e->mu);
     e->slice_density = std::max(e->slice_density, dens);
   }
@@ -777,9 +791,10 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
     // the copy stream must not overwrite text a previous search still reads
     if (w->done) MAG_CUDA(cudaStreamWaitEvent(w->copy_stream, w->done, 0));
     const Plan& P = e->plan;
-    const uint64_t slices = geometry(e, len, 1).num_slices;
+    const SearchGeometry sg = geometry(e, len, 1);
+    const uint64_t slices = sg.num_slices;
     const uint64_t slice_bytes =
-        P.slice_samples * (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
+        sg.slice_samples * (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
     const uint64_t chunk = std::max<uint64_t>(uint64_t(64) << 20, (len + 31) / 32);
     std::vector<SliceRange> ranges;
     uint64_t copied = 0, slices_done = 0;
