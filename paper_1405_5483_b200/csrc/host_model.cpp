@@ -440,7 +440,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       uint32_t chunk = kChunkTarget;
       int direct = 0;
       int roll = 0;
-      uint32_t roll_words = 0, halo = 0;
+      uint32_t roll_words = 0, halo = 0, ddepth = 0;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -551,12 +551,15 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     // staging, the table takes the smem; an occurrence (m >= 2q - 1) always
     // covers one whole aligned sample, at one of q shifts
     for (unsigned q : {16u, 8u}) {
+      // rq.stages selects the ring depth (2..4; single-probe q = 16 tables only)
+      const bool depth_ok = rq.stages == 0 || (q == 16 && rq.stages >= 2 && rq.stages <= 4 && rq.probes <= 1);
       if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
-            (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && rq.stages == 0 && rq.tile_bytes == 0))
+            (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
       const uint32_t warps = q == 8 ? 16 : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16);
       ScanPlan z{};
       z.q = q;
+      z.ddepth = static_cast<uint32_t>(rq.stages);
       const size_t fixed = direct_smem(z, warps) + 1024;
       const size_t room = rq.smem_limit > fixed ? rq.smem_limit - fixed : 0;
       // tables of at most ~64 bits per admitted gram (every CTA loads its copy)
@@ -572,6 +575,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room && (size_t(1) << tb1) < cap_bits) ++tb1;
       for (unsigned H = 1; H <= (q == 8 ? 4u : kMaxProbes) && blocks > 0; ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
+        if (rq.stages != 0 && H > 1) continue;
         const double bits = H == 1 ? std::ldexp(1.0, static_cast<int>(tb1)) : 64.0 * blocks;
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / bits);
         const double p = exact + (1.0 - exact) * std::pow(fill, static_cast<double>(H));
@@ -595,6 +599,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.og = 0;
           best.blocks = H > 1 ? blocks : 0;
           best.tb = H > 1 ? 0 : tb1;
+          best.ddepth = static_cast<uint32_t>(rq.stages);
         }
       }
     }
@@ -667,6 +672,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.probes = best.H;
       sp.blocks = best.H > 1 ? (best.direct ? best.blocks : static_cast<uint32_t>((1ull << best.tb) / 64)) : 0;
       sp.direct = best.direct;
+      sp.ddepth = best.ddepth;
       sp.roll = best.roll;
       best_halo = best.halo;
       if (best.roll) {

@@ -148,6 +148,7 @@ struct ScanPlan {
   uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..kMaxProbes)
   uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
   int direct;             // q = 16 stream kernel (register prefetch, no staging)
+  uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
   uint32_t entry_log2;    // log2(bits per mask entry), 0..6
@@ -205,11 +206,14 @@ struct SmemLayout {
 // of kDirectDepth 1 KiB step buffers (+ mbarriers) per warp.
 constexpr int kDirectDepth = 4;
 constexpr int kDirectMaxWarps = 24;  // direct kernel: up to 768 threads (3-deep rings past 16 warps)
-MAG_HD int direct_depth(uint32_t nwarps) { return nwarps > 16 ? 3 : kDirectDepth; }
+// Ring depth of the direct kernel: the plan's (2..4), 3 past 16 warps.
+MAG_HD int direct_depth(const ScanPlan& p, uint32_t nwarps) {
+  return nwarps > 16 ? 3 : (p.ddepth >= 2 && p.ddepth <= 4 ? static_cast<int>(p.ddepth) : kDirectDepth);
+}
 constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lane
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
-         size_t(nwarps) * direct_depth(nwarps) * (kDirectStep * (p.q == 8 ? 8 : 16) + 16 + 8) + 64;
+         size_t(nwarps) * direct_depth(p, nwarps) * (kDirectStep * (p.q == 8 ? 8 : 16) + 16 + 8) + 64;
 }
 
 // Roll kernel: Bloom words, per-warp ring of kRollDepth slots of

@@ -1369,6 +1369,10 @@ cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, si
     return cudaErrorInvalidValue;
   }
   if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32, 16>(a, stream, grid, smem);
+  if constexpr (H == 1) {  // shallower rings leave room for a 2^20-bit single-probe table
+    if (a.plan.ddepth == 2) return launch_direct_hd<H, 2, 512, 16>(a, stream, grid, smem);
+    if (a.plan.ddepth == 3) return launch_direct_hd<H, 3, 512, 16>(a, stream, grid, smem);
+  }
   return launch_direct_hd<H, kDirectDepth, 512, 16>(a, stream, grid, smem);
 }
 
