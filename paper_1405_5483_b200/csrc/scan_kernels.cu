@@ -1659,6 +1659,12 @@ struct RollScanner {
         if (!live[k]) pr[k] = 0;
         tx[k] = text16(sw, pr[k]);
         key[k] = key_of(tx[k]);
+      }
+      // all slot loads after all expansions: a shuffle of candidate k+1
+      // would otherwise share a scoreboard with candidate k's loads and wait
+      // for them, serialising the round trips
+#pragma unroll
+      for (int k = 0; k < kVK; ++k) {
         const uint32_t slot = key[k] & A.vmask, slot1 = (slot + 1) & A.vmask;
         const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
         hq[k] = live[k] ? __ldg(A.vtab + 2 * slot) : empty;
