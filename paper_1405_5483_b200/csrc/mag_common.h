@@ -221,9 +221,10 @@ MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
 constexpr int kRollDepth = 2;
 constexpr int kRollStep = 2048;   // positions per step: 2 runs of 32 per lane
 MAG_HD uint32_t roll_slot_bytes(uint32_t halo) { return static_cast<uint32_t>(align16(kRollStep + halo)); }
+constexpr int kRollList = 256;     // per-warp list of a step's hit positions (u16)
 MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
   return align16(size_t(words) * 4) + size_t(nwarps) * kRollDepth * roll_slot_bytes(halo) +
-         size_t(nwarps) * kRollDepth * (32 + 8) + 64;
+         size_t(nwarps) * kRollDepth * (32 + 8) + size_t(nwarps) * kRollList * 2 + 64;
 }
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,

@@ -1422,6 +1422,7 @@ struct RollScanner {
   const int lane;
   const uint32_t* bloom;
   uint32_t bloom_s;         // shared-window address of the Bloom words
+  uint16_t* list;           // [kRollList] hit positions of the current step
   uint8_t* slots;
   uint64_t* bars;
   RollDesc* desc;
@@ -1435,8 +1436,9 @@ struct RollScanner {
   bool p_done, p_first;
   uint64_t pol;
 
-  __device__ RollScanner(const ScanArgs& a, const uint32_t* bl, uint8_t* sl, uint64_t* b, RollDesc* d, int l)
-      : A(a), lane(l), bloom(bl), bloom_s(smem_addr(bl)), slots(sl), bars(b), desc(d),
+  __device__ RollScanner(const ScanArgs& a, const uint32_t* bl, uint8_t* sl, uint64_t* b, RollDesc* d,
+                         uint16_t* li, int l)
+      : A(a), lane(l), bloom(bl), bloom_s(smem_addr(bl)), list(li), slots(sl), bars(b), desc(d),
         slot_bytes(roll_slot_bytes(a.back)),
         bq(roll_pow(Q)), fill(0), cands32(0), out(nullptr), p_t(0), p_end(0), p_slice(0), p_done(false),
         p_first(false), pol(policy_evict_first()) {}
@@ -1635,6 +1637,17 @@ struct RollScanner {
     cands32 += c0 + c1;
     if (A.plan.diag & 8) return;
     const uint32_t packed = e0 | (e1 << 16);
+    // Expansion: with at most kRollList hits each lane writes its own hit
+    // positions at its prefix offsets (text order) into the warp's list;
+    // denser steps rank-search the lane masks instead.
+    const bool listed = total <= static_cast<uint32_t>(kRollList);
+    if (listed) {
+      uint32_t idx = e0;
+      for (uint32_t m = h0; m; m &= m - 1) list[idx++] = static_cast<uint16_t>(32 * lane + __ffs(m) - 1);
+      idx = t0 + e1;
+      for (uint32_t m = h1; m; m &= m - 1) list[idx++] = static_cast<uint16_t>(1024 + 32 * lane + __ffs(m) - 1);
+      __syncwarp();
+    }
     for (uint32_t base = 0; base < total; base += 32 * kVK) {
       uint32_t pr[kVK], key[kVK], c[kVK], pid0[kVK];
       uint4 tx[kVK], hq[kVK], bq[kVK], hn[kVK], bn[kVK];
@@ -1643,19 +1656,23 @@ struct RollScanner {
       for (int k = 0; k < kVK; ++k) {
         const uint32_t rank = base + 32 * k + lane;
         live[k] = rank < total;
-        const bool r1 = rank >= t0;
-        const uint32_t rr = r1 ? rank - t0 : rank;
-        const uint32_t sh = r1 ? 16u : 0u;
-        int o = 0;
+        if (listed) {
+          pr[k] = live[k] ? list[rank] : 0u;
+        } else {
+          const bool r1 = rank >= t0;
+          const uint32_t rr = r1 ? rank - t0 : rank;
+          const uint32_t sh = r1 ? 16u : 0u;
+          int o = 0;
 #pragma unroll
-        for (int step = 16; step; step >>= 1) {
-          const uint32_t e = (__shfl_sync(kFull, packed, o + step) >> sh) & 0xffffu;
-          if (e <= rr) o += step;
+          for (int step = 16; step; step >>= 1) {
+            const uint32_t e = (__shfl_sync(kFull, packed, o + step) >> sh) & 0xffffu;
+            if (e <= rr) o += step;
+          }
+          const uint32_t m0 = __shfl_sync(kFull, h0, o), m1 = __shfl_sync(kFull, h1, o);
+          const uint32_t eo = (__shfl_sync(kFull, packed, o) >> sh) & 0xffffu;
+          pr[k] = (r1 ? 1024u : 0u) + 32u * static_cast<uint32_t>(o) +
+                  static_cast<uint32_t>(__fns(r1 ? m1 : m0, 0, static_cast<int>(rr - eo) + 1));
         }
-        const uint32_t m0 = __shfl_sync(kFull, h0, o), m1 = __shfl_sync(kFull, h1, o);
-        const uint32_t eo = (__shfl_sync(kFull, packed, o) >> sh) & 0xffffu;
-        pr[k] = (r1 ? 1024u : 0u) + 32u * static_cast<uint32_t>(o) +
-                static_cast<uint32_t>(__fns(r1 ? m1 : m0, 0, static_cast<int>(rr - eo) + 1));
         if (!live[k]) pr[k] = 0;
         tx[k] = text16(sw, pr[k]);
         key[k] = key_of(tx[k]);
@@ -1761,12 +1778,14 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_roll_kernel(const __gri
   RollDesc* desc = reinterpret_cast<RollDesc*>(p) + static_cast<size_t>(warp) * kRollDepth;
   p += static_cast<size_t>(nw) * kRollDepth * sizeof(RollDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kRollDepth;
+  p += static_cast<size_t>(nw) * kRollDepth * 8;
+  uint16_t* list = reinterpret_cast<uint16_t*>(p) + static_cast<size_t>(warp) * kRollList;
   if ((threadIdx.x & 31) == 0) {
     for (int j = 0; j < kRollDepth; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  RollScanner<Q, H> rs(A, reinterpret_cast<const uint32_t*>(smem), slots, bars, desc, threadIdx.x & 31);
+  RollScanner<Q, H> rs(A, reinterpret_cast<const uint32_t*>(smem), slots, bars, desc, list, threadIdx.x & 31);
   rs.run();
 }
 
