@@ -925,6 +925,10 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
       e[3] = static_cast<uint32_t>(pd.off[i] / 16);
       std::memcpy(e + 4, pd.pattern(i), 16);  // patterns are zero padded to 16 bytes
     }
+    // bit 31 of the len word: the next slot is occupied (the probe run goes on)
+    for (size_t i = 0; i < slots; ++i)
+      if (pt->vtab[8 * i + 1] != 0xffffffffu && pt->vtab[8 * ((i + 1) & pt->vmask) + 1] != 0xffffffffu)
+        pt->vtab[8 * i + 2] |= 0x80000000u;
   }
   // buckets by low key bits, stable within a bucket
   const size_t nb = size_t(1) << sp.bucket_bits;

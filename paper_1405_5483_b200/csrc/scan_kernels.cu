@@ -1585,40 +1585,31 @@ struct RollScanner {
   __device__ __forceinline__ bool slot_match(const uint32_t* sw, uint32_t valid, unsigned long long a,
                                              uint32_t pr, const uint4& t, uint32_t key, const uint4& h,
                                              const uint4& b) const {
-    if (h.x != key || a + h.z > A.n) return false;
-    const uint32_t len = h.z;
+    const uint32_t len = h.z & 0x7fffffffu;
+    if (h.x != key || a + len > A.n) return false;
     const uint32_t d = ((t.x ^ b.x) & key_word_mask(len, 0)) | ((t.y ^ b.y) & key_word_mask(len, 1)) |
                        ((t.z ^ b.z) & key_word_mask(len, 2)) | ((t.w ^ b.w) & key_word_mask(len, 3));
     if (d) return false;
     return len <= 16 || equal_slot(sw, valid, a, pr, h.y, len);
   }
 
-  // Linear-probe run from the key's home slot; slots are consumed in pairs
-  // (h0,b0 = home, h1,b1 = next: both loaded in one round trip), so with a
-  // load factor <= 1/4 nearly every run ends inside the first pair.
+  // Linear-probe run from the key's home slot (h, b already loaded): bit 31
+  // of a slot's len word says whether the next slot is occupied, so with a
+  // load factor <= 1/4 nearly every lookup is one L2 round trip.
   __device__ uint32_t probe(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
                             const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first,
-                            uint4 h0, uint4 b0, uint4 h1, uint4 b1) const {
+                            uint4 h, uint4 b) const {
     uint32_t s = key & A.vmask, c = 0;
-    for (;;) {
-      if (h0.y == 0xffffffffu) break;
-      if (slot_match(sw, valid, a, pr, t, key, h0, b0)) {
-        if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h0.y);
-        if (c == 0 && first) *first = h0.y;
+    while (h.y != 0xffffffffu) {
+      if (slot_match(sw, valid, a, pr, t, key, h, b)) {
+        if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h.y);
+        if (c == 0 && first) *first = h.y;
         ++c;
       }
-      if (h1.y == 0xffffffffu) break;
-      if (slot_match(sw, valid, a, pr, t, key, h1, b1)) {
-        if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h1.y);
-        if (c == 0 && first) *first = h1.y;
-        ++c;
-      }
-      s = (s + 2) & A.vmask;
-      h0 = __ldg(A.vtab + 2 * s);
-      b0 = __ldg(A.vtab + 2 * s + 1);
-      const uint32_t s1 = (s + 1) & A.vmask;
-      h1 = __ldg(A.vtab + 2 * s1);
-      b1 = __ldg(A.vtab + 2 * s1 + 1);
+      if (!(h.z >> 31)) break;
+      s = (s + 1) & A.vmask;
+      h = __ldg(A.vtab + 2 * s);
+      b = __ldg(A.vtab + 2 * s + 1);
     }
     return c;
   }
@@ -1627,7 +1618,7 @@ struct RollScanner {
   // [32 l, 32 l + 32) of lane l) before run 1 ([1024 + 32 l, ...)).  Two
   // candidates per lane per batch, so both verification-slot loads (one L2
   // round trip each) are in flight together.
-  static constexpr int kVK = 2;
+  static constexpr int kVK = 3;
   __device__ void verify_step(const uint32_t* sw, uint32_t valid, unsigned long long t, uint32_t h0,
                               uint32_t h1) {
     const uint32_t c0 = __popc(h0), c1 = __popc(h1);
@@ -1650,7 +1641,7 @@ struct RollScanner {
     }
     for (uint32_t base = 0; base < total; base += 32 * kVK) {
       uint32_t pr[kVK], key[kVK], c[kVK], pid0[kVK];
-      uint4 tx[kVK], hq[kVK], bq[kVK], hn[kVK], bn[kVK];
+      uint4 tx[kVK], hq[kVK], bq[kVK];
       bool live[kVK];
 #pragma unroll
       for (int k = 0; k < kVK; ++k) {
@@ -1682,18 +1673,15 @@ struct RollScanner {
       // for them, serialising the round trips
 #pragma unroll
       for (int k = 0; k < kVK; ++k) {
-        const uint32_t slot = key[k] & A.vmask, slot1 = (slot + 1) & A.vmask;
+        const uint32_t slot = key[k] & A.vmask;
         const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
         hq[k] = live[k] ? __ldg(A.vtab + 2 * slot) : empty;
         bq[k] = live[k] ? __ldg(A.vtab + 2 * slot + 1) : empty;
-        hn[k] = live[k] ? __ldg(A.vtab + 2 * slot1) : empty;
-        bn[k] = live[k] ? __ldg(A.vtab + 2 * slot1 + 1) : empty;
       }
 #pragma unroll
       for (int k = 0; k < kVK; ++k) {
         pid0[k] = 0;
-        c[k] = probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], nullptr, 0, &pid0[k], hq[k], bq[k], hn[k],
-                     bn[k]);
+        c[k] = probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], nullptr, 0, &pid0[k], hq[k], bq[k]);
       }
 #pragma unroll
       for (int k = 0; k < kVK; ++k) {
@@ -1703,9 +1691,9 @@ struct RollScanner {
         if (c[k] == 1) {
           if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], pid0[k]);
         } else if (c[k] > 1) {
-          const uint32_t slot = key[k] & A.vmask, slot1 = (slot + 1) & A.vmask;
+          const uint32_t slot = key[k] & A.vmask;
           probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], out, fill + ex, nullptr, __ldg(A.vtab + 2 * slot),
-                __ldg(A.vtab + 2 * slot + 1), __ldg(A.vtab + 2 * slot1), __ldg(A.vtab + 2 * slot1 + 1));
+                __ldg(A.vtab + 2 * slot + 1));
         }
         fill += tot;
       }

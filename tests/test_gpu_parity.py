@@ -356,3 +356,34 @@ def test_roll_kernel(mag, ref, H):
             d = torch.from_numpy(text).cuda()
             pd = e.prepare_device(d.data_ptr() + 5, n - 5, keep=d)
             assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[5:], pats))
+
+
+def test_concurrent_searches_one_engine(mag, ref):
+    """An engine is immutable and searches on it may run concurrently
+    (engine.hpp:55-56): host threads searching different texts through one
+    engine (per-search pooled workspaces) all get their own exact results."""
+    import threading
+    rng = np.random.default_rng(31)
+    base = (rng.integers(0, 4, 400000) + 65).astype(np.uint8)
+    pats = [base[s:s + 24].tobytes() for s in rng.integers(0, base.size - 24, 200)]
+    texts = [np.roll(base, 7919 * i).copy() for i in range(6)]
+    want = [as_pairs(*ref.ac(t, pats)) for t in texts]
+    for kernel in ("auto", "roll", "staged"):
+        e = mag.Engine(pats, scan_kernel=kernel)
+        got = [None] * len(texts)
+        errs = []
+
+        def run(i):
+            try:
+                for _ in range(3):
+                    got[i] = e.search(texts[i]).pairs()
+            except Exception as ex:  # pragma: no cover - surfaced below
+                errs.append(ex)
+
+        th = [threading.Thread(target=run, args=(i,)) for i in range(len(texts))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert not errs, errs
+        assert got == want, kernel
