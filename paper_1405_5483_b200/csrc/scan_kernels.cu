@@ -1183,8 +1183,10 @@ struct DirectScanner {
       const uint2 blk = static_cast<const uint2*>(table)[bloom_block(h, A.plan.blocks)];
       return bloom_admits_w<H>(blk.x, blk.y, h);
     } else {
+      // word h >> (37 - tb), bit (h >> (32 - tb)) & 31 via a wrap-mode funnel shift
       const uint32_t idx = h >> (32 - A.plan.table_bits);
-      return !((static_cast<const uint32_t*>(table)[idx >> 5] >> (idx & 31u)) & 1u);
+      const uint32_t wd = static_cast<const uint32_t*>(table)[idx >> 5];
+      return !(__funnelshift_r(wd, wd, idx) & 1u);
     }
   }
 
@@ -1214,19 +1216,18 @@ struct DirectScanner {
     // all lookups first (independent shared-memory loads in flight together)
 #pragma unroll
     for (int i = 0; i < kPer; ++i) hit[i] = admits(h[i]);
+    if (lim < kStep) {  // the text's last step: samples past the end never hit
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) hit[i] = hit[i] && static_cast<uint32_t>(lane + 32 * i) < lim;
+    }
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      hit[i] = hit[i] && static_cast<uint32_t>(lane + 32 * i) < lim;
       cands32 += hit[i] ? 1u : 0u;
-      uint32_t key = h[i];
-      if (!A.plan.key_gram) {
-        const uint32_t wl = A.plan.wkey_len;
-        key = key_words(v[i].x & key_word_mask(wl, 0), v[i].y & key_word_mask(wl, 1),
-                        v[i].z & key_word_mask(wl, 2), v[i].w & key_word_mask(wl, 3));
-      }
+      // the window key is the sample's gram hash (direct plans: key_gram)
+      const uint32_t key = h[i];
       pend_k[i] = key;
       const uint32_t sb = lb ? screen_bit(key, lb) : 0u;
-      pend_b[i] = sb & 31u;
+      pend_b[i] = sb;  // resolve() shifts in wrap mode: bit sb & 31
       // the screen word is only consumed by resolve() one step later
       uint32_t w = 0;
       if (hit[i] && !count_only) w = (lb && !(A.plan.diag & 128)) ? __ldg(A.l2map + (sb >> 5)) : ~0u;
@@ -1237,7 +1238,7 @@ struct DirectScanner {
   __device__ __forceinline__ void resolve() {
     uint32_t surv = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) surv |= ((pend_w[i] >> pend_b[i]) & 1u) << i;
+    for (int i = 0; i < kPer; ++i) surv |= (__funnelshift_r(pend_w[i], pend_w[i], pend_b[i]) & 1u) << i;
     if (__any_sync(kFull, surv != 0)) {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 32u * W * i);
