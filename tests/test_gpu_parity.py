@@ -387,3 +387,50 @@ def test_concurrent_searches_one_engine(mag, ref):
             t.join()
         assert not errs, errs
         assert got == want, kernel
+
+
+@pytest.mark.parametrize("q", [8, 16])
+def test_direct_kernel(mag, ref, port, q):
+    """The aligned-sample kernel (forced), both sample widths: texts of every
+    length class around its 128-sample step (odd 8-byte sample counts
+    included), m = 2q-1 (the shortest admissible) up to patterns longer than
+    any staged halo, duplicates, dense plants, misaligned device text; the
+    candidate counter equals the restated hashed machine's."""
+    rng = np.random.default_rng(50 + q)
+    step = 128 * q
+    sizes = [0, 5, q, 2 * q - 1, step - 8, step, step + 8, step + 24, 3 * step + 8, 2048 * q + 40, 250_000]
+    for it, n in enumerate(sizes):
+        m = int(rng.choice([2 * q - 1, 2 * q, 3 * q, 64]))
+        sig = int(rng.choice([2, 4, 20]))
+        text = (rng.integers(0, sig, n) + 65).astype(np.uint8)
+        pats = []
+        for _ in range(int(rng.integers(1, 200))):
+            L = m + int(rng.integers(0, 3))
+            if n > L and rng.random() < 0.6:
+                s0 = int(rng.integers(0, n - L + 1))
+                pats.append(text[s0:s0 + L].tobytes())
+            else:
+                pats.append((rng.integers(0, sig, L) + 65).astype(np.uint8).tobytes())
+        if n > 2000 and it % 2:
+            pats.append(text[n - 1500:n].tobytes())
+            pats.append(pats[0])
+        text = text.copy()
+        for _ in range(n // 64):
+            p = pats[int(rng.integers(0, len(pats)))]
+            if len(p) < n:
+                s0 = int(rng.integers(0, n - len(p) + 1))
+                text[s0:s0 + len(p)] = np.frombuffer(p, dtype=np.uint8)
+        e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED)
+        pl = e.plan()
+        assert pl["direct"] == 1 and pl["q"] == q, pl
+        got, met = gpu_pairs(e, text)
+        assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
+        P = port.params(variant=0, gram_mode=1, q=q, k=1, table_bits=pl["table_bits"], word_bits=1,
+                        probes=pl["probes"], blocks=pl["blocks"])
+        _, _, reads, cands = port.search(text, pats, P)
+        assert (met.filter_reads, met.candidates) == (reads, cands), (n, m, pl)
+        if n > 64:
+            import torch
+            d = torch.from_numpy(text).cuda()
+            pd = e.prepare_device(d.data_ptr() + 3, n - 3, keep=d)
+            assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[3:], pats))
