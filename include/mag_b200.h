@@ -35,6 +35,7 @@ typedef struct mag_options_ex {
   int device;      /* CUDA device ordinal, -1 = current */
   int probes;      /* hashed: table entries probed per gram, 0 = auto */
   int scan_kernel; /* mag_scan_kernel: which scan the planner may pick, 0 = auto */
+  int cluster;     /* direct kernel: 0 = auto, 1 = never, 8 = table shared by 8-CTA clusters (DSMEM) */
 } mag_options_ex;
 
 /* Scan kernels of hashed plans (mag_options_ex.scan_kernel). */
@@ -71,6 +72,7 @@ typedef struct mag_plan_info {
   uint32_t blocks;      /* probes >= 2: 64-entry table blocks */
   int direct;           /* q = 16 stream kernel */
   int roll;             /* dense rolling-hash scan (every position, q-byte prefix Bloom) */
+  int cluster;          /* direct: CTAs per cluster sharing the table through DSMEM (0 = none) */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

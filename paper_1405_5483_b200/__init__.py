@@ -64,6 +64,7 @@ class _OptionsEx(C.Structure):  # mag_b200.h
         ("base", _Options), ("gram_mode", C.c_int), ("table_bits", C.c_int),
         ("word_bits", C.c_int), ("tile_bytes", C.c_int), ("warps", C.c_int),
         ("stages", C.c_int), ("device", C.c_int), ("probes", C.c_int), ("scan_kernel", C.c_int),
+        ("cluster", C.c_int),
     ]
 
 
@@ -83,7 +84,7 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("bucket_bits", C.c_uint32), ("tile_bytes", C.c_uint32), ("halo", C.c_uint32),
         ("warps", C.c_uint32), ("stages", C.c_uint32), ("smem_bytes", C.c_size_t),
         ("predicted_candidates_per_byte", C.c_double), ("probes", C.c_uint32),
-        ("blocks", C.c_uint32), ("direct", C.c_int), ("roll", C.c_int),
+        ("blocks", C.c_uint32), ("direct", C.c_int), ("roll", C.c_int), ("cluster", C.c_int),
     ]
 
 
@@ -295,7 +296,7 @@ class Engine:
     def __init__(self, patterns: Sequence[bytes], variant="mag", mapping="auto", lowbits=0, q=0, k=0,
                  sigma_prime=0, threads=1, histogram_sample: Optional[bytes] = None,
                  gram_mode=GRAM_AUTO, table_bits=0, word_bits=0, tile_bytes=0, warps=0, stages=0,
-                 device=-1, probes=0, scan_kernel="auto"):
+                 device=-1, probes=0, scan_kernel="auto", cluster=0):
         L = lib()
         self._h = C.c_void_p()
         opts = _OptionsEx()
@@ -313,6 +314,7 @@ class Engine:
         opts.tile_bytes, opts.warps, opts.stages, opts.device = int(tile_bytes), int(warps), int(stages), int(device)
         opts.probes = int(probes)
         opts.scan_kernel = KERNELS[scan_kernel] if isinstance(scan_kernel, str) else int(scan_kernel)
+        opts.cluster = int(cluster)
         bufs = [_as_u8(p) for p in patterns]
         n = len(bufs)
         ptrs = (C.POINTER(C.c_uint8) * max(n, 1))(*[_u8ptr(b) for b in bufs])

@@ -543,6 +543,9 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     rq.warps = opts.warps;
     rq.stages = opts.stages;
     rq.probes = opts.probes;
+    rq.cluster = opts.cluster;
+    if (opts.cluster != 0 && opts.cluster != 1 && opts.cluster != 8)
+      return fail(MAG_ERR_BAD_CONFIG, "cluster must be 0 (auto), 1 or 8");
     rq.kernel = opts.scan_kernel;
     if (opts.scan_kernel < 0 || opts.scan_kernel > 3)
       return fail(MAG_ERR_BAD_CONFIG, "unknown scan kernel " + std::to_string(opts.scan_kernel));
@@ -635,6 +638,7 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->blocks = P.sp.blocks;
   out->direct = P.sp.direct;
   out->roll = P.sp.roll;
+  out->cluster = static_cast<int>(P.sp.cluster);
   return MAG_OK;
 }
 

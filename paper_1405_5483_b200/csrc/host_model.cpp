@@ -246,6 +246,7 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
                  kCostPf = 15,       // shared-memory prefilter test
                  kCostDirectHit = 120,  // direct kernel: a filter hit issues one L2 screen load
+                 kCostClusterLookup = 25,  // direct: DSMEM table lookup, per byte (W = 16), measured
                  kCostRollPos = 24,   // roll kernel: roll + one Bloom word per position
                  kCostRollProbe = 1.5,  // each Bloom probe
                  kCostRollBatch = 6,  // a verification batch (expansion, keys, slot loads) per 64 bytes of lane work
@@ -440,7 +441,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       uint32_t chunk = kChunkTarget;
       int direct = 0;
       int roll = 0;
-      uint32_t roll_words = 0, halo = 0, ddepth = 0;
+      uint32_t roll_words = 0, halo = 0, ddepth = 0, cluster = 0;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -608,6 +609,36 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.blocks = H > 1 ? blocks : 0;
           best.tb = H > 1 ? 0 : tb1;
           best.ddepth = H > 1 ? static_cast<uint32_t>(rq.stages) : depth1;
+          best.cluster = 0;
+        }
+      }
+      // single-probe table spread over a cluster of 8 CTAs (8x the bits,
+      // read through distributed shared memory).  Opt-in only (cluster = 8):
+      // measured on B200 a remote lookup per sample caps the scan near
+      // 1.3 TB/s (cfg2 1,348 vs 4,154 GB/s; cfg4 1,216 vs 2,261 GB/s even
+      // with 4.6x fewer candidates), far below the local 2^20-bit table
+      if (q == 16 && depth1 == 2 && (rq.probes <= 1) && warps == 16 && rq.cluster == 8) {
+        const unsigned tbc = tb1 + 3;
+        const double fill = 1.0 - std::exp(-distinct / std::ldexp(1.0, static_cast<int>(tbc)));
+        const double cpb = (exact + (1.0 - exact) * fill) / q;
+        const double cost = kStagedScale * (kCostSample + 2 * kCostProbeBit) / q + kCostClusterLookup +
+                            cpb * (kCostDirectHit + 0.008 * (kCostCand + kCostProbe + hits * kCostCompare));
+        if ((rq.cluster == 8 || cost < best.cost * 0.999) && tbc <= 26) {
+          best.cost = cost;
+          best.q = q;
+          best.k = 1;
+          best.mp = 1;
+          best.H = 1;
+          best.pf = 0;
+          best.chunk = kChunkTarget;
+          best.va = false;
+          best.cpb = cpb;
+          best.direct = 1;
+          best.og = 0;
+          best.blocks = 0;
+          best.tb = tbc;
+          best.ddepth = depth1;
+          best.cluster = 8;
         }
       }
     }
@@ -681,6 +712,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.blocks = best.H > 1 ? (best.direct ? best.blocks : static_cast<uint32_t>((1ull << best.tb) / 64)) : 0;
       sp.direct = best.direct;
       sp.ddepth = best.ddepth;
+      sp.cluster = best.cluster;
       sp.roll = best.roll;
       best_halo = best.halo;
       if (best.roll) {

@@ -75,6 +75,7 @@ struct PlanRequest {
   int tile_bytes = 0, warps = 0, stages = 0;  // tile_bytes: chunk bytes target; stages: ring
   int probes = 0;            // hashed: 0 auto
   int kernel = 0;            // mag_scan_kernel: 0 auto, 1 staged, 2 direct, 3 roll
+  int cluster = 0;           // direct: 0 auto, 1 never, 8 force the cluster-shared table
   size_t smem_limit = 232448;  // sm_100 max dynamic shared memory per CTA
 };
 

@@ -148,6 +148,7 @@ struct ScanPlan {
   uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..kMaxProbes)
   uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
   int direct;             // q = 16 stream kernel (register prefetch, no staging)
+  uint32_t cluster;       // direct: CTAs per cluster sharing the table through DSMEM (0/1 = none)
   uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
@@ -212,7 +213,7 @@ MAG_HD int direct_depth(const ScanPlan& p, uint32_t nwarps) {
 }
 constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lane
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
-  return align16(p.table_bytes) + align16(size_t(nwarps) * kProbeCap * 8) +
+  return align16(p.table_bytes / (p.cluster > 1 ? p.cluster : 1)) + align16(size_t(nwarps) * kProbeCap * 8) +
          size_t(nwarps) * direct_depth(p, nwarps) * (kDirectStep * (p.q == 8 ? 8 : 16) + 16 + 8) + 64;
 }
 

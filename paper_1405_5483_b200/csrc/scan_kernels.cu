@@ -1088,12 +1088,13 @@ struct __align__(16) DirectDesc {
   uint32_t t, slice, lim_flags, pad;
 };
 
-template <int H, int DEPTH, int W>
+template <int H, int DEPTH, int W, int CL = 1>
 struct DirectScanner {
   static_assert(W == 8 || W == 16, "sample width");
   const ScanArgs& A;
   const int lane;
   const void* table;
+  uint32_t table_s;   // shared-window address of the (local slice of the) table
   uint2* pq;
   uint8_t* slots;     // [DEPTH][kDirectStep * W] staged samples
   uint64_t* bars;     // [kDirectDepth]
@@ -1111,7 +1112,8 @@ struct DirectScanner {
 
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
-      : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
+      : A(a), lane(l), table(tab), table_s(smem_addr(tab)), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0),
+        cands32(0),
         pbase_t(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
     for (int i = 0; i < kPer; ++i) pend_w[i] = pend_b[i] = pend_k[i] = 0;
     pend_pos = 0;
@@ -1179,7 +1181,21 @@ struct DirectScanner {
   }
 
   __device__ __forceinline__ bool admits(uint32_t h) const {
-    if constexpr (H > 1) {
+    if constexpr (CL > 1) {
+      // the table is split over the cluster: slice = top log2(CL) index bits,
+      // read through distributed shared memory (mapa + ld.shared::cluster)
+      constexpr uint32_t kLog = CL == 8 ? 3 : (CL == 4 ? 2 : 1);
+      const uint32_t idx = h >> (32 - A.plan.table_bits);
+      const uint32_t lbits = A.plan.table_bits - kLog;
+      const uint32_t rank = idx >> lbits, off = idx & ((1u << lbits) - 1u);
+      const uint32_t laddr = table_s + (off >> 5) * 4u;
+      uint32_t raddr, wd;
+      asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(rank));
+      // not volatile: the table is constant during the scan, so the compiler
+      // may issue a step's four remote loads together
+      asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(wd) : "r"(raddr));
+      return !(__funnelshift_r(wd, wd, off) & 1u);
+    } else if constexpr (H > 1) {
       const uint2 blk = static_cast<const uint2*>(table)[bloom_block(h, A.plan.blocks)];
       return bloom_admits_w<H>(blk.x, blk.y, h);
     } else {
@@ -1318,17 +1334,28 @@ struct DirectScanner {
   }
 };
 
-template <int H, int DEPTH, int NT, int W>
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+template <int H, int DEPTH, int NT, int W, int CL = 1>
 __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
   // let the dependent gather grid launch early (it waits for our completion)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(128) uint8_t smem[];
-  const size_t tbytes = align16(A.plan.table_bytes);
+  // CL > 1: this CTA holds slice cluster_rank() of the table
+  const size_t tbytes = align16(A.plan.table_bytes / CL);
   {
-    const uint4* src = static_cast<const uint4*>(A.table);
+    const uint4* src = static_cast<const uint4*>(A.table) + (CL > 1 ? cluster_rank() * (tbytes / 16) : 0);
     uint4* dst = reinterpret_cast<uint4*>(smem);
     for (size_t i = threadIdx.x; i < tbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();  // every slice loaded before any remote read
   }
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint8_t* p = smem + tbytes;
@@ -1344,8 +1371,9 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  DirectScanner<H, DEPTH, W> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
+  DirectScanner<H, DEPTH, W, CL> ds(A, smem, pq, slots, bars, desc, threadIdx.x & 31);
   ds.run();
+  if constexpr (CL > 1) cluster_sync_all();  // keep this slice alive until the cluster is done
 }
 
 template <int H, int DEPTH, int NT, int W>
@@ -1363,6 +1391,49 @@ cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, s
   return cudaGetLastError();
 }
 
+// Cluster launch: CL CTAs share one table through distributed shared
+// memory; the grid is a whole number of clusters (idle CTAs just sync).
+template <int CL>
+cudaError_t launch_direct_cluster(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
+  auto k = mag_direct_kernel<1, 2, 512, 16, CL>;
+  static int configured = -1;
+  if (configured != static_cast<int>(smem)) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = static_cast<int>(smem);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(a.nwarps * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // as many clusters as can be co-resident (GPC packing), none beyond
+  static int resident = -1, resident_smem = -1;
+  if (resident_smem != static_cast<int>(smem)) {
+    cfg.gridDim = dim3(CL * 64);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess || nc <= 0) {
+      (void)cudaGetLastError();
+      nc = 148 / CL;
+    }
+    resident = nc;
+    resident_smem = static_cast<int>(smem);
+  }
+  const int want = (grid + CL - 1) / CL;
+  cfg.gridDim = dim3(static_cast<unsigned>(CL * (want < resident ? want : resident)));
+  (void)cudaGetLastError();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k, a);
+  if (e != cudaSuccess) return e;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 template <int H>
 cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
   if (a.plan.q == 8) {  // 8-byte samples (m >= 15)
@@ -1371,6 +1442,8 @@ cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, si
   }
   if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32, 16>(a, stream, grid, smem);
   if constexpr (H == 1) {  // shallower rings leave room for a 2^20-bit single-probe table
+    if (a.plan.cluster == 8 && a.plan.ddepth == 2 && a.nwarps == 16)
+      return launch_direct_cluster<8>(a, stream, grid, smem);
     if (a.plan.ddepth == 2) return launch_direct_hd<H, 2, 512, 16>(a, stream, grid, smem);
     if (a.plan.ddepth == 3) return launch_direct_hd<H, 3, 512, 16>(a, stream, grid, smem);
   }

@@ -389,9 +389,10 @@ def test_concurrent_searches_one_engine(mag, ref):
         assert got == want, kernel
 
 
-@pytest.mark.parametrize("q", [8, 16])
-def test_direct_kernel(mag, ref, port, q):
-    """The aligned-sample kernel (forced), both sample widths: texts of every
+@pytest.mark.parametrize("q,cluster", [(8, 1), (16, 1), (16, 8)])
+def test_direct_kernel(mag, ref, port, q, cluster):
+    """The aligned-sample kernel (forced), both sample widths, and the table
+    shared by 8-CTA clusters through distributed shared memory: texts of every
     length class around its 128-sample step (odd 8-byte sample counts
     included), m = 2q-1 (the shortest admissible) up to patterns longer than
     any staged halo, duplicates, dense plants, misaligned device text; the
@@ -420,9 +421,9 @@ def test_direct_kernel(mag, ref, port, q):
             if len(p) < n:
                 s0 = int(rng.integers(0, n - len(p) + 1))
                 text[s0:s0 + len(p)] = np.frombuffer(p, dtype=np.uint8)
-        e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED)
+        e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED, cluster=cluster)
         pl = e.plan()
-        assert pl["direct"] == 1 and pl["q"] == q, pl
+        assert pl["direct"] == 1 and pl["q"] == q and pl["cluster"] == (8 if cluster == 8 else 0), pl
         got, met = gpu_pairs(e, text)
         assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
         P = port.params(variant=0, gram_mode=1, q=q, k=1, table_bits=pl["table_bits"], word_bits=1,
