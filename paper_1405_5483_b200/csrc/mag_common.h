@@ -214,7 +214,7 @@ MAG_HD int direct_depth(const ScanPlan& p, uint32_t nwarps) {
 constexpr int kDirectStep = 128;  // samples per step (2 KiB of text), 4 per lane
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes / (p.cluster > 1 ? p.cluster : 1)) + align16(size_t(nwarps) * kProbeCap * 8) +
-         size_t(nwarps) * direct_depth(p, nwarps) * (kDirectStep * (p.q == 8 ? 8 : 16) + 16 + 8) + 64;
+         size_t(nwarps) * direct_depth(p, nwarps) * (kDirectStep * 16 + 16 + 8) + 64;
 }
 
 // Roll kernel: Bloom words, per-warp ring of kRollDepth slots of

@@ -1096,14 +1096,16 @@ struct DirectScanner {
   const void* table;
   uint32_t table_s;   // shared-window address of the (local slice of the) table
   uint2* pq;
-  uint8_t* slots;     // [DEPTH][kDirectStep * W] staged samples
+  uint8_t* slots;     // [DEPTH][kStepBytes] staged samples
   uint64_t* bars;     // [kDirectDepth]
   DirectDesc* desc;   // [kDirectDepth]
   uint32_t pqn, fill, cands32;
   uint32_t pbase_t;   // first sample of the current slice
   uint64_t* out;
-  static constexpr uint32_t kStep = kDirectStep;
-  static constexpr int kPer = kDirectStep / 32;  // samples per lane per step
+  // a step is 2 KiB of text: 128 16-byte or 256 8-byte samples
+  static constexpr uint32_t kStepBytes = kDirectStep * 16;
+  static constexpr uint32_t kStep = kStepBytes / W;
+  static constexpr int kPer = kStep / 32;  // samples per lane per step
   uint32_t pend_w[kPer], pend_b[kPer], pend_k[kPer], pend_pos;  // screen loads in flight
   // producer cursor (warp-uniform)
   uint32_t p_t, p_left;
@@ -1156,14 +1158,14 @@ struct DirectScanner {
         const uint32_t lim = p_left < kStep ? p_left : kStep;
         d.t = p_t;
         d.slice = first ? slice : desc[j == 0 ? DEPTH - 1 : j - 1].slice;
-        d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= kStep ? 2u : 0u)) << 8);
+        d.lim_flags = lim | ((4u | (first ? 1u : 0u) | (p_left <= kStep ? 2u : 0u)) << 16);
         d.pad = 0;
         // (dep & A.zero) == 0, but only at run time: the byte count, hence the
         // TMA issue, data-depends on every word loaded from the slot
         // bulk copies move whole 16-byte units: an odd 8-byte sample count
         // (the text's last step) leaves one sample for a plain load
         const uint32_t total = W * lim, bulk = total & ~15u;
-        uint8_t* dst = slots + static_cast<size_t>(j) * kDirectStep * W;
+        uint8_t* dst = slots + static_cast<size_t>(j) * kStepBytes;
         const uint8_t* src = A.text + static_cast<uint64_t>(W) * p_t;
         if (total != bulk)
           *reinterpret_cast<uint2*>(dst + bulk) = __ldg(reinterpret_cast<const uint2*>(src + bulk));
@@ -1267,7 +1269,7 @@ struct DirectScanner {
   // shared-memory loads are in flight): a new slice resets the output
   // cursor, otherwise the previous step's screen loads are resolved.
   __device__ __forceinline__ void begin(const DirectDesc& d) {
-    if ((d.lim_flags >> 8) & 1u) {
+    if ((d.lim_flags >> 16) & 1u) {
       fill = 0;
       pqn = 0;
       pbase_t = d.t;
@@ -1278,7 +1280,7 @@ struct DirectScanner {
   }
 
   __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
-    const uint32_t lim = d.lim_flags & 0xffu, flags = d.lim_flags >> 8;
+    const uint32_t lim = d.lim_flags & 0xffffu, flags = d.lim_flags >> 16;
     pend_pos = W * (d.t - pbase_t) + W * lane;
     filter(v, h, lim);
     if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
@@ -1298,7 +1300,7 @@ struct DirectScanner {
 #pragma unroll 1
     while (true) {
       const DirectDesc d = desc[j];
-      if (!(d.lim_flags & 0x400u)) break;  // steps are issued in order: first invalid = end
+      if (!(d.lim_flags & (4u << 16))) break;  // steps are issued in order: first invalid = end
       mbar_wait(bars + j, (phase >> j) & 1u);
       phase ^= 1u << j;
       uint4 v[kPer];
@@ -1306,9 +1308,9 @@ struct DirectScanner {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
         if constexpr (W == 16) {
-          v[i] = reinterpret_cast<const uint4*>(slots + static_cast<size_t>(j) * kDirectStep * W)[32 * i + lane];
+          v[i] = reinterpret_cast<const uint4*>(slots + static_cast<size_t>(j) * kStepBytes)[32 * i + lane];
         } else {
-          const uint2 x = reinterpret_cast<const uint2*>(slots + static_cast<size_t>(j) * kDirectStep * W)[32 * i + lane];
+          const uint2 x = reinterpret_cast<const uint2*>(slots + static_cast<size_t>(j) * kStepBytes)[32 * i + lane];
           v[i] = make_uint4(x.x, x.y, 0u, 0u);
         }
       }
@@ -1361,8 +1363,8 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
   uint8_t* p = smem + tbytes;
   uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kProbeCap;
   p += align16(size_t(nw) * kProbeCap * 8);
-  uint8_t* slots = p + static_cast<size_t>(warp) * DEPTH * kDirectStep * W;
-  p += size_t(nw) * DEPTH * kDirectStep * W;
+  uint8_t* slots = p + static_cast<size_t>(warp) * DEPTH * kDirectStep * 16;
+  p += size_t(nw) * DEPTH * kDirectStep * 16;
   DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
   p += size_t(nw) * DEPTH * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
