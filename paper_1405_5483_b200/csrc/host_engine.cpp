@@ -239,7 +239,7 @@ struct SearchGeometry {
 uint64_t slice_samples_for(const mag_engine* e, uint64_t samples) {
   const Plan& P = e->plan;
   const uint64_t unit =
-      P.sp.roll ? kRollStep : (P.sp.direct ? kDirectStep * 16 / P.sp.q : P.chunk_samples);  // one kernel step
+      P.sp.roll ? kRollStep : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);  // one step
   const uint64_t warps = static_cast<uint64_t>(e->sm_count) * P.nwarps * 4;
   uint64_t want = (samples + warps - 1) / warps;
   want = (want + unit - 1) / unit * unit;

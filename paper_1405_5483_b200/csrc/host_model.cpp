@@ -754,6 +754,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.m_prime = static_cast<uint32_t>(std::min<size_t>(L / sp.k, w / sp.k));
   set_entry_geometry(sp);
   finish_geometry(pd, rq, P);
+  if (sp.direct) {  // direct kernel: slices of whole steps, ~32 KiB of text
+    const uint64_t step = direct_step_bytes(sp.q) / sp.q;
+    P->slice_samples = step * std::max<uint64_t>(1, 32768 / direct_step_bytes(sp.q));
+  }
   if (sp.roll) {  // roll kernel geometry: 2 KiB steps, 16 steps per slice
     P->chunk_samples = kRollStep;
     P->slice_samples = static_cast<uint64_t>(kRollStep) * 16;

@@ -1102,8 +1102,8 @@ struct DirectScanner {
   uint32_t pqn, fill, cands32;
   uint32_t pbase_t;   // first sample of the current slice
   uint64_t* out;
-  // a step is 2 KiB of text: 128 16-byte or 256 8-byte samples
-  static constexpr uint32_t kStepBytes = kDirectStep * 16;
+  // a step: 160 16-byte samples (2.5 KiB) or 256 8-byte samples (2 KiB)
+  static constexpr uint32_t kStepBytes = W == 16 ? 2560u : 2048u;
   static constexpr uint32_t kStep = kStepBytes / W;
   static constexpr int kPer = kStep / 32;  // samples per lane per step
   uint32_t pend_w[kPer], pend_b[kPer], pend_k[kPer], pend_pos;  // screen loads in flight
@@ -1218,7 +1218,7 @@ struct DirectScanner {
   __device__ __forceinline__ void push(bool hit, uint32_t key, uint32_t pos) {
     const unsigned bal = __ballot_sync(kFull, hit);
     if (!bal) return;
-    if (pqn + __popc(bal) > kProbeCap) flush();
+    if (pqn + __popc(bal) > kDirectProbeCap) flush();
     if (hit) pq[pqn + __popc(bal & ((1u << lane) - 1u))] = make_uint2(key, pos);
     __syncwarp();
     pqn += __popc(bal);
@@ -1361,10 +1361,10 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
   }
   const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   uint8_t* p = smem + tbytes;
-  uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kProbeCap;
-  p += align16(size_t(nw) * kProbeCap * 8);
-  uint8_t* slots = p + static_cast<size_t>(warp) * DEPTH * kDirectStep * 16;
-  p += size_t(nw) * DEPTH * kDirectStep * 16;
+  uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kDirectProbeCap;
+  p += align16(size_t(nw) * kDirectProbeCap * 8);
+  uint8_t* slots = p + static_cast<size_t>(warp) * DEPTH * direct_step_bytes(W);
+  p += size_t(nw) * DEPTH * direct_step_bytes(W);
   DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
   p += size_t(nw) * DEPTH * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
