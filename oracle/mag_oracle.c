@@ -105,7 +105,6 @@ uint32_t mo_gram_hash(const uint8_t* p, unsigned q) {
                x[3] * 0x27D4EB2Fu;
   h ^= h >> 15;
   h *= 0x2C1B3C6Du;
-  h ^= h >> 12;
   return h;
 }
 

@@ -39,10 +39,11 @@ MAG_HD uint64_t pack_match(uint64_t offset, uint32_t pid) {
 // Filter-side gram hash over q <= 16 raw bytes given as four little-endian
 // words with bytes past q already zeroed.  Must match mo_gram_hash().
 MAG_HD uint32_t hash_gram_words(uint32_t x0, uint32_t x1, uint32_t x2, uint32_t x3) {
+  // no final xorshift: table slots take the top bits (already mixed by the
+  // multiply) and the L2 screen's low bits measured as selective without it
   uint32_t h = x0 * 0x9E3779B1u + x1 * 0x85EBCA77u + x2 * 0xC2B2AE3Du + x3 * 0x27D4EB2Fu;
   h ^= h >> 15;
   h *= 0x2C1B3C6Du;
-  h ^= h >> 12;
   return h;
 }
 
