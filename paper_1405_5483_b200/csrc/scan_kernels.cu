@@ -57,17 +57,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
@@ -935,22 +924,15 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
 }
 
 // ============================================================ direct kernel
-// q = 16, k = m' = 1 hashed plans (the DNA r = 10k shape): sample t is the
-// aligned 16-byte word text[16t, 16t + 16), so warps stream samples straight
-// from HBM with coalesced 16-byte loads, kDirectDepth steps of 64 samples
-// prefetched in registers — no shared-memory staging at all, which leaves
-// the whole shared memory to a multi-probe filter table.  A hit's window key
-// is the same 16 bytes (hashed from the registers); keys queue per warp and
-// are screened against the L2 bitmap, survivors walk their bucket and are
-// compared against the text in global memory.  Output: per-slice ordered
-// staging, exactly as the staged kernel.
-__device__ __forceinline__ uint4 ld_stream16(const uint8_t* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
+// q = W (16 or 8), k = m' = 1 hashed plans (cfg1-cfg4 shapes, m >= 2W - 1):
+// sample t is the aligned W-byte word text[W t, W t + W), which every
+// occurrence covers at one of W shifts.  Each warp streams its slices
+// through a small ring of TMA-filled steps (2.5 KiB / 2 KiB), so shared
+// memory goes to the filter table (2^19-2^20 bits, or a blocked multi-probe
+// table).  A hit's window key is the sample's own gram hash; its L2 screen
+// word is loaded at once and resolved a step later, survivors queue per warp,
+// walk their (pattern, shift) bucket and are compared against the text in
+// global memory.  Output: per-slice ordered staging, as every scan kernel.
 
 // Exact compare of pattern pid against text[a, a + len) in global memory:
 // 16 pattern bytes at a time against two aligned 16-byte text loads
@@ -1227,7 +1209,7 @@ struct DirectScanner {
   // Filter the lane's kPer samples of a step; a filter hit issues its L2
   // screen load now and is resolved one step later (resolve()), so the L2
   // round trip overlaps the next step's filtering instead of stalling.
-  __device__ __forceinline__ void filter(const uint4 (&v)[kPer], const uint32_t (&h)[kPer], uint32_t lim) {
+  __device__ __forceinline__ void filter(const uint32_t (&h)[kPer], uint32_t lim) {
     const uint32_t lb = A.plan.l2_bits;
     const bool count_only = A.plan.diag & 8;  // diagnostics: no screen / verification
     bool hit[kPer];
@@ -1282,7 +1264,7 @@ struct DirectScanner {
   __device__ __forceinline__ void process(const DirectDesc& d, const uint4 (&v)[kPer], const uint32_t (&h)[kPer]) {
     const uint32_t lim = d.lim_flags & 0xffffu, flags = d.lim_flags >> 16;
     pend_pos = W * (d.t - pbase_t) + W * lane;
-    filter(v, h, lim);
+    filter(h, lim);
     if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
     if (flags & 2u) {
       resolve();
