@@ -358,7 +358,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   const size_t m = pd.m;
   const unsigned w = rq.word_bits > 0 ? std::min(64, rq.word_bits) : 64;
 
-  uint32_t best_halo = 0;  // roll plans: staged bytes past a step
+  uint32_t best_halo = 0;   // roll plans: staged bytes past a step
+  uint32_t best_warps = 0;  // direct plans: warps per CTA the planner chose
   const bool reference_mode = rq.gram_mode == 0 ||
                               (rq.gram_mode < 0 && (rq.q || rq.k || rq.sigma_prime ||
                                                      rq.mapping != -1));
@@ -441,7 +442,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       uint32_t chunk = kChunkTarget;
       int direct = 0;
       int roll = 0;
-      uint32_t roll_words = 0, halo = 0, ddepth = 0, cluster = 0;
+      uint32_t roll_words = 0, halo = 0, ddepth = 0, cluster = 0, warps = 0;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -557,7 +558,12 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
             (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
-      const uint32_t warps = q == 8 ? 16 : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 16);
+      // W = 16 sets that saturate the table (cfg4: ~3 grams per table bit)
+      // run 14 warps: measured 2,619 vs 1,934 GB/s at 16 (fewer outstanding
+      // L2 screen loads), while sparse sets (cfg2) keep 16 (4,670 vs 4,582)
+      const bool dense = keys * q > 0.7 * std::ldexp(1.0, 20);
+      const uint32_t warps = q == 8 ? 16
+                                    : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : (dense ? 14 : 16));
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)
@@ -565,7 +571,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         ScanPlan z{};
         z.q = q;
         z.ddepth = depth;
-        const size_t fixed = direct_smem(z, warps) + 1024;
+        const size_t fixed = direct_smem(z, warps);  // the kernel has no static shared memory
         return rq.smem_limit > fixed ? rq.smem_limit - fixed : size_t(0);
       };
       const uint32_t depth1 = rq.stages ? static_cast<uint32_t>(rq.stages) : (q == 16 && warps <= 16 ? 2u : 0u);
@@ -582,8 +588,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       // single probe: largest power-of-two table that fits
       unsigned tb1 = 6;
       while (tb1 < 26 && (size_t(1) << (tb1 + 1)) / 8 <= room1 && (size_t(1) << tb1) < cap_bits) ++tb1;
-      for (unsigned H = 1; H <= (q == 8 ? 4u : kMaxProbes) && blocks > 0; ++H) {
+      for (unsigned H = 1; H <= (q == 8 ? 4u : kMaxProbes); ++H) {
         if (rq.probes > 0 && H != static_cast<unsigned>(rq.probes)) continue;
+        if (H > 1 && blocks == 0) break;  // multi-probe tables run 4-deep rings: no room left
+        if (H == 1 && room1 < 2048) continue;
         if (rq.stages != 0 && H > 1) continue;
         const double bits = H == 1 ? std::ldexp(1.0, static_cast<int>(tb1)) : 64.0 * blocks;
         const double fill = 1.0 - std::exp(-static_cast<double>(H) * distinct / bits);
@@ -610,6 +618,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.tb = H > 1 ? 0 : tb1;
           best.ddepth = H > 1 ? static_cast<uint32_t>(rq.stages) : depth1;
           best.cluster = 0;
+          best.warps = warps;
         }
       }
       // single-probe table spread over a cluster of 8 CTAs (8x the bits,
@@ -617,7 +626,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       // measured on B200 a remote lookup per sample caps the scan near
       // 1.3 TB/s (cfg2 1,348 vs 4,154 GB/s; cfg4 1,216 vs 2,261 GB/s even
       // with 4.6x fewer candidates), far below the local 2^20-bit table
-      if (q == 16 && depth1 == 2 && (rq.probes <= 1) && warps == 16 && rq.cluster == 8) {
+      if (q == 16 && depth1 == 2 && (rq.probes <= 1) && warps <= 16 && rq.cluster == 8) {
         const unsigned tbc = tb1 + 3;
         const double fill = 1.0 - std::exp(-distinct / std::ldexp(1.0, static_cast<int>(tbc)));
         const double cpb = (exact + (1.0 - exact) * fill) / q;
@@ -639,6 +648,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.tb = tbc;
           best.ddepth = depth1;
           best.cluster = 8;
+          best.warps = warps;
         }
       }
     }
@@ -713,6 +723,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.direct = best.direct;
       sp.ddepth = best.ddepth;
       sp.cluster = best.cluster;
+      best_warps = best.warps;
       sp.roll = best.roll;
       best_halo = best.halo;
       if (best.roll) {
@@ -780,7 +791,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   } else {
     sp.table_in_smem = sp.verify_all ? 0 : 1;
     if (sp.direct)
-      P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, sp.q == 8 ? 16u : kDirectMaxWarps) : 16;
+      P->nwarps = best_warps ? best_warps
+                             : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, sp.q == 8 ? 16u : kDirectMaxWarps) : 16u);
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;

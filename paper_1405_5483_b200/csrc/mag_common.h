@@ -213,9 +213,9 @@ MAG_HD int direct_depth(const ScanPlan& p, uint32_t nwarps) {
   return nwarps > 16 ? 3 : (p.ddepth >= 2 && p.ddepth <= 4 ? static_cast<int>(p.ddepth) : kDirectDepth);
 }
 constexpr int kDirectStep = 128;  // samples per W=16 step before round 1's 2.5 KiB steps
-// Text bytes per direct-kernel step: 160 16-byte samples (5 per lane) or
-// 256 8-byte samples (8 per lane).
-MAG_HD uint32_t direct_step_bytes(uint32_t q) { return q == 8 ? 2048u : 2560u; }
+// Text bytes per direct-kernel step: 256 16-byte samples or 256 8-byte
+// samples (8 per lane either way).
+MAG_HD uint32_t direct_step_bytes(uint32_t q) { return q == 8 ? 2048u : 4096u; }
 constexpr int kDirectProbeCap = 64;  // direct kernel: screened window keys queued per warp
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
   return align16(p.table_bytes / (p.cluster > 1 ? p.cluster : 1)) + align16(size_t(nwarps) * kDirectProbeCap * 8) +

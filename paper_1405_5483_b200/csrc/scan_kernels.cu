@@ -1084,8 +1084,8 @@ struct DirectScanner {
   uint32_t pqn, fill, cands32;
   uint32_t pbase_t;   // first sample of the current slice
   uint64_t* out;
-  // a step: 160 16-byte samples (2.5 KiB) or 256 8-byte samples (2 KiB)
-  static constexpr uint32_t kStepBytes = W == 16 ? 2560u : 2048u;
+  // a step: 256 16-byte samples (4 KiB) or 256 8-byte samples (2 KiB)
+  static constexpr uint32_t kStepBytes = W == 16 ? 4096u : 2048u;
   static constexpr uint32_t kStep = kStepBytes / W;
   static constexpr int kPer = kStep / 32;  // samples per lane per step
   uint32_t pend_w[kPer], pend_b[kPer], pend_k[kPer], pend_pos;  // screen loads in flight
@@ -1426,7 +1426,7 @@ cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, si
   }
   if (a.nwarps > 16) return launch_direct_hd<H, 3, kDirectMaxWarps * 32, 16>(a, stream, grid, smem);
   if constexpr (H == 1) {  // shallower rings leave room for a 2^20-bit single-probe table
-    if (a.plan.cluster == 8 && a.plan.ddepth == 2 && a.nwarps == 16)
+    if (a.plan.cluster == 8 && a.plan.ddepth == 2 && a.nwarps <= 16)
       return launch_direct_cluster<8>(a, stream, grid, smem);
     if (a.plan.ddepth == 2) return launch_direct_hd<H, 2, 512, 16>(a, stream, grid, smem);
     if (a.plan.ddepth == 3) return launch_direct_hd<H, 3, 512, 16>(a, stream, grid, smem);
