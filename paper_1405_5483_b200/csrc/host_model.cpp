@@ -559,11 +559,12 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
             (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
       // W = 16 sets that saturate the table (cfg4: ~3 grams per table bit)
-      // run 14 warps: measured 2,619 vs 1,934 GB/s at 16 (fewer outstanding
-      // L2 screen loads), while sparse sets (cfg2) keep 16 (4,670 vs 4,582)
+      // run 15 warps: measured 13/14/15/16 warps = 2,551/2,604/2,686/1,934
+      // GB/s (a 16th warp leaves L1 ~17 KB; the screen/bucket loads go
+      // through it), while sparse sets (cfg2) keep 16 (4,670 vs 4,582 at 14)
       const bool dense = keys * q > 0.7 * std::ldexp(1.0, 20);
       const uint32_t warps = q == 8 ? 16
-                                    : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : (dense ? 14 : 16));
+                                    : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : (dense ? 15 : 16));
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)
