@@ -443,7 +443,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       int direct = 0;
       int roll = 0;
       uint32_t roll_words = 0, halo = 0, ddepth = 0, cluster = 0, warps = 0;
-      bool screen_l1 = true;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -559,12 +558,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
             (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
-      // W = 16 runs 15 warps: measured best for both shapes (cfg4 13/14/15/16
-      // warps = 2,551/2,604/2,686/1,934 GB/s; cfg2 15 vs 16 = 4,855 vs 4,786).
-      // Table-saturating sets (cfg4: ~3 grams per table bit) screen through
-      // L1; sparse ones bypass it (see scan_kernels.cu ld_screen).
+      // W = 16 sets that saturate the table (cfg4: ~3 grams per table bit)
+      // run 15 warps: measured 13/14/15/16 warps = 2,551/2,604/2,686/1,934
+      // GB/s (a 16th warp leaves L1 ~17 KB; the screen/bucket loads go
+      // through it), while sparse sets (cfg2) keep 16 (4,670 vs 4,582 at 14)
       const bool dense = keys * q > 0.7 * std::ldexp(1.0, 20);
-      const uint32_t warps = q == 8 ? 16 : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : 15);
+      const uint32_t warps = q == 8 ? 16
+                                    : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kDirectMaxWarps) : (dense ? 15 : 16));
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)
@@ -620,7 +620,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.ddepth = H > 1 ? static_cast<uint32_t>(rq.stages) : depth1;
           best.cluster = 0;
           best.warps = warps;
-          best.screen_l1 = dense;
         }
       }
       // single-probe table spread over a cluster of 8 CTAs (8x the bits,
@@ -725,7 +724,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.direct = best.direct;
       sp.ddepth = best.ddepth;
       sp.cluster = best.cluster;
-      sp.screen_l1 = best.screen_l1 ? 1 : 0;
       best_warps = best.warps;
       sp.roll = best.roll;
       best_halo = best.halo;

@@ -150,7 +150,6 @@ struct ScanPlan {
   uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
   int direct;             // q = 16 stream kernel (register prefetch, no staging)
   uint32_t cluster;       // direct: CTAs per cluster sharing the table through DSMEM (0/1 = none)
-  int screen_l1;          // direct: L2 screen loads allocate in L1 (re-read screen words)
   uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)

@@ -934,17 +934,6 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
 // walk their (pattern, shift) bucket and are compared against the text in
 // global memory.  Output: per-slice ordered staging, as every scan kernel.
 
-// L2 screen word without L1 allocation: for sparse gram sets (DNA) screen
-// words are almost never re-read, and L1 is what shared memory leaves.
-// Table-saturating sets over repetitive text (cfg4) re-read them, so their
-// plans keep L1 (plan.screen_l1): measured 2,686 vs 1,453 GB/s there, while
-// cfg2 gains 4,670 -> 4,855 GB/s without it.
-__device__ __forceinline__ uint32_t ld_screen(const uint32_t* p) {
-  uint32_t v;
-  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
 // Exact compare of pattern pid against text[a, a + len) in global memory:
 // 16 pattern bytes at a time against two aligned 16-byte text loads
 // (independent, one round trip per piece) realigned with funnel shifts.
@@ -1241,10 +1230,7 @@ struct DirectScanner {
       pend_b[i] = sb;  // resolve() shifts in wrap mode: bit sb & 31
       // the screen word is only consumed by resolve() one step later
       uint32_t w = 0;
-      if (hit[i] && !count_only)
-        w = (lb && !(A.plan.diag & 128))
-                ? (A.plan.screen_l1 ? __ldg(A.l2map + (sb >> 5)) : ld_screen(A.l2map + (sb >> 5)))
-                : ~0u;
+      if (hit[i] && !count_only) w = (lb && !(A.plan.diag & 128)) ? __ldg(A.l2map + (sb >> 5)) : ~0u;
       pend_w[i] = w;
     }
   }
