@@ -934,6 +934,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
 // walk their (pattern, shift) bucket and are compared against the text in
 // global memory.  Output: per-slice ordered staging, as every scan kernel.
 
+// Read-only load under a predicate (0 when off): one predicated LDG, no branch.
+__device__ __forceinline__ uint32_t ld_nc_pred(const uint32_t* p, bool on) {
+  uint32_t v;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t"
+      "@q ld.global.nc.u32 %0, [%1];\n\t}"
+      : "=r"(v)
+      : "l"(p), "r"(static_cast<uint32_t>(on)));
+  return v;
+}
+
 // Exact compare of pattern pid against text[a, a + len) in global memory:
 // 16 pattern bytes at a time against two aligned 16-byte text loads
 // (independent, one round trip per piece) realigned with funnel shifts.
@@ -1212,6 +1222,7 @@ struct DirectScanner {
   __device__ __forceinline__ void filter(const uint32_t (&h)[kPer], uint32_t lim) {
     const uint32_t lb = A.plan.l2_bits;
     const bool count_only = A.plan.diag & 8;  // diagnostics: no screen / verification
+    const bool screen = lb && !(A.plan.diag & 128);
     bool hit[kPer];
     // all lookups first (independent shared-memory loads in flight together)
 #pragma unroll
@@ -1228,9 +1239,21 @@ struct DirectScanner {
       pend_k[i] = key;
       const uint32_t sb = lb ? screen_bit(key, lb) : 0u;
       pend_b[i] = sb;  // resolve() shifts in wrap mode: bit sb & 31
-      // the screen word is only consumed by resolve() one step later
-      uint32_t w = 0;
-      if (hit[i] && !count_only) w = (lb && !(A.plan.diag & 128)) ? __ldg(A.l2map + (sb >> 5)) : ~0u;
+      // the screen word is only consumed by resolve() one step later.  W = 16
+      // plans (a quarter to most samples hit: cfg2/cfg4) issue it as one
+      // predicated load, no branch per sample (cfg2 +5%); W = 8 plans (rare
+      // hits: cfg1/cfg3) branch around it, which skips whole warps
+      const bool want = hit[i] && !count_only;
+      uint32_t w;
+      if constexpr (W == 16) {
+        if (screen)
+          w = ld_nc_pred(A.l2map + (sb >> 5), want);
+        else
+          w = want ? ~0u : 0u;
+      } else {
+        w = 0;
+        if (want) w = screen ? __ldg(A.l2map + (sb >> 5)) : ~0u;
+      }
       pend_w[i] = w;
     }
   }
