@@ -30,12 +30,13 @@ typedef struct mag_options_ex {
   int table_bits;  /* hashed: log2 mask entries; 0 = auto; -1 = no filter (verify all) */
   int word_bits;   /* w of the reference machine (filter.hpp:34); 0 = 64 */
   int tile_bytes;  /* 0 = auto */
-  int warps;       /* consumer warps per CTA, 0 = auto (<= 16) */
+  int warps;       /* scanning warps per CTA, 0 = auto (<= 15 staged / W=16 direct, <= 16 W=8 / roll);
+                      every CTA adds one gather warp */
   int stages;      /* TMA ring depth, 0 = auto */
   int device;      /* CUDA device ordinal, -1 = current */
   int probes;      /* hashed: table entries probed per gram, 0 = auto */
   int scan_kernel; /* mag_scan_kernel: which scan the planner may pick, 0 = auto */
-  int cluster;     /* direct kernel: 0 = auto, 1 = never, 8 = table shared by 8-CTA clusters (DSMEM) */
+  int cluster;     /* 0 or 1 (kept for ABI stability; the cluster-shared table of round 1 was retired) */
 } mag_options_ex;
 
 /* Scan kernels of hashed plans (mag_options_ex.scan_kernel). */
@@ -72,7 +73,7 @@ typedef struct mag_plan_info {
   uint32_t blocks;      /* probes >= 2: 64-entry table blocks */
   int direct;           /* q = 16 stream kernel */
   int roll;             /* dense rolling-hash scan (every position, q-byte prefix Bloom) */
-  int cluster;          /* direct: CTAs per cluster sharing the table through DSMEM (0 = none) */
+  int cluster;          /* always 0 (kept for ABI stability) */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);
@@ -84,7 +85,10 @@ MAG_API mag_status mag_prepare_device_text(const mag_engine* engine, const uint8
 /* Enqueue a search on `cuda_stream` (a cudaStream_t; NULL = legacy default)
  * and return at once.  The handle materialises (waits, copies the sorted
  * matches to the host) on first use by mag_matches_count/get/metrics or by
- * mag_matches_sync; destroying it unmaterialised is allowed. */
+ * mag_matches_sync; destroying it unmaterialised is allowed.  The prepared
+ * text (and the device memory behind mag_prepare_device_text) must outlive
+ * the handle's materialisation: a slice that overflowed its staging is
+ * searched again then. */
 MAG_API mag_status mag_search_prepared_async(const mag_engine* engine,
                                              const mag_prepared* prepared, void* cuda_stream,
                                              mag_matches** out);

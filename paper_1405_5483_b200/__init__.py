@@ -213,10 +213,16 @@ class Metrics:
 
 
 class Matches:
-    """Sorted (offset, pattern_index) occurrences (mag.h:111-122)."""
+    """Sorted (offset, pattern_index) occurrences (mag.h:111-122).
 
-    def __init__(self, handle: int):
+    A pending (asynchronous) handle keeps the prepared text it searches
+    alive until it is closed: materialising may search that text again
+    (staging overflow), so the device text must outlive it (mag_b200.h).
+    """
+
+    def __init__(self, handle: int, keep=None):
         self._h = C.c_void_p(handle)
+        self._keep = keep
 
     def __len__(self) -> int:
         return int(lib().mag_matches_count(self._h))
@@ -251,6 +257,7 @@ class Matches:
         if self._h:
             lib().mag_matches_destroy(self._h)
             self._h = C.c_void_p()
+        self._keep = None
 
     def __del__(self):
         try:
@@ -290,7 +297,8 @@ class Engine:
     sigma_prime, threads, histogram_sample) plus the GPU extras of
     ``mag_options_ex`` (gram_mode, table_bits, word_bits, tile_bytes, warps,
     stages, device, probes, scan_kernel; device=-2 builds the host tables
-    only, no upload).
+    only, no upload).  ``warps`` counts scanning warps; every CTA adds one
+    gather warp.
     """
 
     def __init__(self, patterns: Sequence[bytes], variant="mag", mapping="auto", lowbits=0, q=0, k=0,
@@ -358,12 +366,12 @@ class Engine:
     def search_prepared(self, prepared: Prepared) -> Matches:
         h = C.c_void_p()
         _check(lib().mag_search_prepared(self._h, prepared._h, C.byref(h)))
-        return Matches(h.value)
+        return Matches(h.value, keep=prepared)
 
     def search_prepared_async(self, prepared: Prepared, stream: int = 0) -> Matches:
         h = C.c_void_p()
         _check(lib().mag_search_prepared_async(self._h, prepared._h, C.c_void_p(stream), C.byref(h)))
-        return Matches(h.value)
+        return Matches(h.value, keep=prepared)
 
     def search(self, text) -> Matches:
         """prepare + search (mag_search): host text in, sorted matches out."""

@@ -56,17 +56,23 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // Per-search device scratch, pooled per engine.  `done` orders reuse on the
 // device (a later search waits for it with cudaStreamWaitEvent).
 struct Workspace {
-  // two halves of counters[8] | tickets[kMaxLaunch]: a search uses half
-  // `parity` and its compaction kernel zeroes the other half for the next
-  // search on this workspace (no memset launch per search)
+  // two halves of counters[8] | tickets[kMaxLaunch] | exits[kMaxLaunch]: a
+  // search uses half `parity` and the last warp of its final launch zeroes
+  // the other half for the next search on this workspace (no memset launch
+  // per search).  `dirty`: a search failed half-way; both halves are
+  // cleared before the next one.
   unsigned long long* ctrl = nullptr;
   uint32_t parity = 0;
-  uint32_t* counts = nullptr;          // per-slice match counts
-  size_t counts_cap = 0;
+  bool dirty = false;
+  uint32_t epoch = 0;                  // tag of the last search in slice_state
+  uint64_t* slice_state = nullptr;     // per slice: epoch << 32 | count
+  uint64_t* incl = nullptr;            // per slice: inclusive prefix of counts
+  size_t slices_cap = 0;
   uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
   uint64_t* out = nullptr;             // sorted matches (same capacity)
   size_t out_cap = 0;
-  unsigned long long* h_ctr = nullptr;  // pinned copy of counters[8]
+  unsigned long long* h_ctr = nullptr;  // mapped pinned counters[8], written by the kernel
+  unsigned long long* d_hctr = nullptr; // its device alias
   uint8_t* text = nullptr;              // device copy of host text (mag_search)
   size_t text_cap = 0;
   cudaStream_t copy_stream = nullptr;
@@ -79,7 +85,8 @@ struct Workspace {
   ~Workspace() {
     cudaSetDevice(device);
     if (ctrl) cudaFree(ctrl);
-    if (counts) cudaFree(counts);
+    if (slice_state) cudaFree(slice_state);
+    if (incl) cudaFree(incl);
     if (staging) cudaFree(staging);
     if (out) cudaFree(out);
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -227,19 +234,27 @@ void release(const mag_engine* e, std::unique_ptr<Workspace> w) {
 }
 
 constexpr size_t kCounters = 8;
-constexpr size_t kCtrlWords = kCounters + kMaxLaunch;
+constexpr size_t kCtrlWords = kCounters + 2 * kMaxLaunch;
 
 struct SearchGeometry {
-  uint64_t samples, slice_samples, num_slices, slice_cap;
+  uint64_t samples, slice_samples, tail_samples, big_slices, num_slices, slice_cap;
+  uint32_t bps;  // text bytes per sample
 };
+
+uint64_t bytes_per_sample(const Plan& P) {
+  return P.sp.verify_all || P.sp.overlapping ? 1 : static_cast<uint64_t>(P.sp.q) * P.sp.k;
+}
+
+uint64_t step_unit(const Plan& P) {
+  return P.sp.roll ? kRollStep : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);
+}
 
 // Slices are the warps' work items: the plan's size, but small texts get
 // smaller slices (whole kernel steps) so that every warp of the grid has
 // about four of them.
 uint64_t slice_samples_for(const mag_engine* e, uint64_t samples) {
   const Plan& P = e->plan;
-  const uint64_t unit =
-      P.sp.roll ? kRollStep : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);  // one step
+  const uint64_t unit = step_unit(P);
   const uint64_t warps = static_cast<uint64_t>(e->sm_count) * P.nwarps * 4;
   uint64_t want = (samples + warps - 1) / warps;
   want = (want + unit - 1) / unit * unit;
@@ -250,8 +265,18 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
   const Plan& P = e->plan;
   SearchGeometry g;
   g.samples = filter_reads(P, n);
+  g.bps = static_cast<uint32_t>(bytes_per_sample(P));
   g.slice_samples = slice_samples_for(e, g.samples);
-  g.num_slices = (g.samples + g.slice_samples - 1) / g.slice_samples;
+  // The last wave of the grid runs tail slices 8x finer (about one big slice
+  // per scanning warp), so the warps run out of work together.
+  const uint64_t unit = step_unit(P);
+  g.tail_samples = std::min<uint64_t>(g.slice_samples,
+                                      std::max<uint64_t>(unit, (g.slice_samples / 8 + unit - 1) / unit * unit));
+  const uint64_t tail = std::min<uint64_t>(g.samples / 2,
+                                           static_cast<uint64_t>(e->sm_count) * P.nwarps * g.slice_samples);
+  g.big_slices = g.samples > tail ? (g.samples - tail) / g.slice_samples : 0;
+  const uint64_t rest = g.samples - g.big_slices * g.slice_samples;
+  g.num_slices = g.big_slices + (rest + g.tail_samples - 1) / g.tail_samples;
   if (cap_override) {
     g.slice_cap = cap_override;
   } else {
@@ -266,22 +291,61 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
     const double guess = std::max(dens * static_cast<double>(g.slice_samples) * 1.25, bytes / 128);
     g.slice_cap = std::max<uint64_t>(64, static_cast<uint64_t>(guess) + 32);
   }
+  g.slice_cap = (g.slice_cap + 15) / 16 * 16;  // slices never share a 128-byte line
   return g;
 }
 
-mag_status ensure_ws(Workspace* w, const SearchGeometry& g) {
+ScanArgs geometry_args(const SearchGeometry& g) {
+  ScanArgs a{};
+  a.samples = g.samples;
+  a.slice_samples = g.slice_samples;
+  a.big_slices = g.big_slices;
+  a.tail_samples = g.tail_samples;
+  a.num_slices = g.num_slices;
+  return a;
+}
+
+// Slices [0, k) whose last sample ends at most `bytes` bytes into the text.
+uint64_t slices_ending_by(const SearchGeometry& g, uint64_t bytes) {
+  const ScanArgs a = geometry_args(g);
+  uint64_t lo = 0, hi = g.num_slices;  // answer in [lo, hi]
+  while (lo < hi) {
+    const uint64_t mid = lo + (hi - lo + 1) / 2;  // is slice mid-1 covered?
+    if (slice_t1(a, mid - 1) * g.bps <= bytes)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+mag_status ensure_ws(Workspace* w, const SearchGeometry& g, cudaStream_t st) {
   if (!w->done) MAG_CUDA(cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming));
-  if (!w->h_ctr) MAG_CUDA(cudaMallocHost(&w->h_ctr, kCounters * sizeof(unsigned long long)));
+  if (!w->h_ctr) {
+    MAG_CUDA(cudaHostAlloc(&w->h_ctr, kCounters * sizeof(unsigned long long), cudaHostAllocMapped));
+    std::memset(w->h_ctr, 0, kCounters * sizeof(unsigned long long));
+    MAG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&w->d_hctr), w->h_ctr, 0));
+  }
   if (!w->ctrl) {
     MAG_CUDA(cudaMalloc(&w->ctrl, 2 * kCtrlWords * sizeof(unsigned long long)));
-    MAG_CUDA(cudaMemset(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long)));
-    w->parity = 0;
+    w->dirty = true;
   }
-  if (w->counts_cap < std::max<uint64_t>(1, g.num_slices)) {
-    if (w->counts) MAG_CUDA(cudaFree(w->counts));
-    w->counts = nullptr;
-    w->counts_cap = std::max<uint64_t>(1, g.num_slices);
-    MAG_CUDA(cudaMalloc(&w->counts, w->counts_cap * sizeof(uint32_t)));
+  if (w->dirty) {  // new, or a search failed half-way: both halves from zero
+    MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long), st));
+    w->parity = 0;
+    w->dirty = false;
+  }
+  if (w->slices_cap < std::max<uint64_t>(1, g.num_slices)) {
+    if (w->slice_state) MAG_CUDA(cudaFree(w->slice_state));
+    if (w->incl) MAG_CUDA(cudaFree(w->incl));
+    w->slice_state = w->incl = nullptr;
+    w->slices_cap = 0;
+    const size_t cap = std::max<uint64_t>(1, g.num_slices);
+    MAG_CUDA(cudaMalloc(&w->slice_state, cap * sizeof(uint64_t)));
+    MAG_CUDA(cudaMalloc(&w->incl, cap * sizeof(uint64_t)));
+    // epoch 0 is never a search's tag: fresh states read "not published"
+    MAG_CUDA(cudaMemsetAsync(w->slice_state, 0, cap * sizeof(uint64_t), st));
+    w->slices_cap = cap;
   }
   const size_t cap = std::max<size_t>(1, g.num_slices * g.slice_cap);
   if (w->out_cap < cap) {
@@ -301,76 +365,96 @@ struct SliceRange {
   cudaEvent_t wait;  // may be null
 };
 
-// Enqueue one complete search over device text: zero the control words, run
-// the fused kernel over the slice ranges, gather the staged slices, copy the
-// counters back (pinned), record ws->done.  All on `st`.
+// Enqueue one complete search over device text: the fused kernel over the
+// slice ranges (one launch per range, each after its range's wait event);
+// the final launch's last warp leaves the counters in the mapped host copy
+// and clears the next search's control words; record ws->done.  All on `st`.
 mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_text, uint64_t n,
                           const uint32_t* d_codes, cudaStream_t st,
                           const std::vector<SliceRange>& ranges, uint64_t cap_override = 0) {
   const Plan& P = e->plan;
   const SearchGeometry g = geometry(e, n, cap_override);
-  mag_status s = ensure_ws(w, g);
+  mag_status s = ensure_ws(w, g, st);
   if (s != MAG_OK) return s;
+  w->dirty = true;  // until every launch of this search is enqueued
   w->num_slices = g.num_slices;
   w->slice_cap = g.slice_cap;
   w->slice_samples = g.slice_samples;
+  if (++w->epoch == 0) w->epoch = 1;
   unsigned long long* counters = w->ctrl + w->parity * kCtrlWords;
   unsigned long long* next_ctrl = w->ctrl + (w->parity ^ 1u) * kCtrlWords;
-  w->parity ^= 1u;
-  if (g.num_slices) {
-    ScanArgs a{};
-    a.plan = P.sp;
-    if (const char* d = std::getenv("MAG_B200_DIAG")) a.plan.diag = std::atoi(d);  // profiling only
-    a.text = d_text;
-    a.n = n;
-    a.codes = d_codes;
-    a.table = e->d_table;
-    a.prefilter = e->d_prefilter;
-    a.bucket_start = e->d_bucket_start;
-    a.l2map = e->d_l2map;
-    a.bucket_entries = reinterpret_cast<const uint2*>(e->d_entries);
-    a.vtab = reinterpret_cast<const uint4*>(e->d_vtab);
-    a.vmask = e->ptab.vmask;
-    a.pat_bytes = e->d_pat_bytes;
-    a.pat_off = e->d_pat_off;
-    a.pat_len = e->d_pat_len;
-    a.map = e->d_map;
-    a.samples = g.samples;
-    a.slice_samples = g.slice_samples;
-    a.chunk_samples = P.chunk_samples;
-    a.back = P.back;
-    a.slot_bytes = P.slot_bytes;
-    a.full_bytes = P.full_bytes;
-    a.ring = P.ring;
-    a.nwarps = P.nwarps;
-    a.num_slices = g.num_slices;
-    a.staging = w->staging;
-    a.slice_cap = static_cast<uint32_t>(std::min<uint64_t>(g.slice_cap, 0xffffffffu));
-    a.slice_count = w->counts;
-    a.counters = counters;
-    size_t li = 0;
-    for (const SliceRange& r : ranges) {
-      if (r.wait) MAG_CUDA(cudaStreamWaitEvent(st, r.wait, 0));
-      if (r.end <= r.begin) continue;
-      a.slice_begin = r.begin;
-      a.slice_end = r.end;
-      if (li >= kMaxLaunch) return fail(MAG_ERR_INTERNAL, "too many scan launches for one search");
-      a.ticket = counters + kCounters + li++;
-      const uint64_t ctas = (r.end - r.begin + P.nwarps - 1) / P.nwarps;
-      const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
-      MAG_CUDA(timed_launch(a, st, grid));
-    }
-    const int cgrid = static_cast<int>(std::min<uint64_t>(
-        std::max<uint64_t>(1, g.num_slices / 8), static_cast<uint64_t>(e->sm_count)));
-    a.reset = next_ctrl;
-    a.reset_words = static_cast<uint32_t>(kCtrlWords);
-    MAG_CUDA(launch_compact(a, w->out, w->out_cap, st, cgrid));
-  } else {
-    MAG_CUDA(cudaMemsetAsync(next_ctrl, 0, kCtrlWords * sizeof(unsigned long long), st));
+  ScanArgs a = geometry_args(g);
+  a.plan = P.sp;
+#ifdef MAG_B200_DIAGNOSTICS
+  if (const char* d = std::getenv("MAG_B200_DIAG")) a.plan.diag = std::atoi(d);  // profiling builds only
+#else
+  a.plan.diag = 0;
+#endif
+  a.text = d_text;
+  a.n = n;
+  a.codes = d_codes;
+  a.table = e->d_table;
+  a.prefilter = e->d_prefilter;
+  a.bucket_start = e->d_bucket_start;
+  a.l2map = e->d_l2map;
+  a.bucket_entries = reinterpret_cast<const uint2*>(e->d_entries);
+  a.vtab = reinterpret_cast<const uint4*>(e->d_vtab);
+  a.vmask = e->ptab.vmask;
+  a.pat_bytes = e->d_pat_bytes;
+  a.pat_off = e->d_pat_off;
+  a.pat_len = e->d_pat_len;
+  a.map = e->d_map;
+  a.chunk_samples = P.chunk_samples;
+  a.back = P.back;
+  a.slot_bytes = P.slot_bytes;
+  a.full_bytes = P.full_bytes;
+  a.ring = P.ring;
+  a.nwarps = P.nwarps;
+  a.staging = w->staging;
+  a.slice_cap = static_cast<uint32_t>(std::min<uint64_t>(g.slice_cap, 0xfffffff0u));
+  a.epoch = w->epoch;
+  a.slice_state = w->slice_state;
+  a.incl = w->incl;
+  a.out = w->out;
+  a.out_cap = w->out_cap;
+  a.counters = counters;
+  a.host_ctr = w->d_hctr;
+  a.reset = next_ctrl;
+  a.reset_words = static_cast<uint32_t>(kCtrlWords);
+  // the last non-empty range is the final launch (an empty search still
+  // launches once, so the counters get published)
+  size_t last = ranges.size();
+  for (size_t i = 0; i < ranges.size(); ++i)
+    if (ranges[i].end > ranges[i].begin) last = i;
+  size_t li = 0;
+  auto launch = [&](uint64_t begin, uint64_t end, bool final_launch) -> mag_status {
+    if (li >= kMaxLaunch) return fail(MAG_ERR_INTERNAL, "too many scan launches for one search");
+    a.slice_begin = begin;
+    a.slice_end = end;
+    a.ticket = counters + kCounters + li;
+    a.exits = counters + kCounters + kMaxLaunch + li;
+    ++li;
+    const uint64_t ctas = std::max<uint64_t>(1, (end - begin + P.nwarps - 1) / P.nwarps);
+    const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
+    a.launch_warps = static_cast<uint32_t>(grid) * (P.nwarps + 1);
+    a.final_launch = final_launch ? 1u : 0u;
+    MAG_CUDA(timed_launch(a, st, grid));
+    return MAG_OK;
+  };
+  for (size_t i = 0; i < ranges.size(); ++i) {
+    const SliceRange& r = ranges[i];
+    if (r.wait) MAG_CUDA(cudaStreamWaitEvent(st, r.wait, 0));
+    if (r.end <= r.begin) continue;
+    s = launch(r.begin, r.end, i == last);
+    if (s != MAG_OK) return s;
   }
-  MAG_CUDA(cudaMemcpyAsync(w->h_ctr, counters, kCounters * sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, st));
+  if (last == ranges.size()) {
+    s = launch(0, 0, true);
+    if (s != MAG_OK) return s;
+  }
   MAG_CUDA(cudaEventRecord(w->done, st));
+  w->parity ^= 1u;
+  w->dirty = false;
   return MAG_OK;
 }
 
@@ -387,15 +471,16 @@ mag_status materialize(mag_matches* m) {
   cudaSetDevice(e->device);
   Workspace* w = m->ws.get();
   MAG_CUDA(cudaEventSynchronize(w->done));
-  unsigned long long total = w->h_ctr[2], maxc = w->h_ctr[3];
+  volatile unsigned long long* hc = w->h_ctr;  // written by the kernel (mapped)
+  unsigned long long total = hc[2], maxc = hc[3];
   if (maxc > w->slice_cap) {
     const uint64_t slices = w->num_slices;
     mag_status s = enqueue_search(e, w, m->d_text, m->n, m->d_codes, m->stream,
                                   {SliceRange{0, slices, nullptr}}, maxc);
     if (s != MAG_OK) return s;
     MAG_CUDA(cudaEventSynchronize(w->done));
-    total = w->h_ctr[2];
-    maxc = w->h_ctr[3];
+    total = hc[2];
+    maxc = hc[3];
   }
   {
     const double dens = static_cast<double>(maxc) / static_cast<double>(std::max<uint64_t>(1, w->slice_samples));
@@ -406,8 +491,7 @@ mag_status materialize(mag_matches* m) {
   if (total)
     MAG_CUDA(cudaMemcpy(m->keys.data(), w->out, total * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   m->metrics.filter_reads = filter_reads(e->plan, m->n);
-  m->metrics.candidates =
-      e->plan.sp.verify_all ? analytic_candidates(e->plan, m->n) : w->h_ctr[1];
+  m->metrics.candidates = e->plan.sp.verify_all ? analytic_candidates(e->plan, m->n) : hc[1];
   m->pending = false;
   release(e, std::move(m->ws));
   return MAG_OK;
@@ -545,8 +629,8 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     rq.stages = opts.stages;
     rq.probes = opts.probes;
     rq.cluster = opts.cluster;
-    if (opts.cluster != 0 && opts.cluster != 1 && opts.cluster != 8)
-      return fail(MAG_ERR_BAD_CONFIG, "cluster must be 0 (auto), 1 or 8");
+    if (opts.cluster != 0 && opts.cluster != 1)
+      return fail(MAG_ERR_BAD_CONFIG, "cluster must be 0 (auto) or 1 (the cluster-shared table was retired)");
     rq.kernel = opts.scan_kernel;
     if (opts.scan_kernel < 0 || opts.scan_kernel > 3)
       return fail(MAG_ERR_BAD_CONFIG, "unknown scan kernel " + std::to_string(opts.scan_kernel));
@@ -639,7 +723,7 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->blocks = P.sp.blocks;
   out->direct = P.sp.direct;
   out->roll = P.sp.roll;
-  out->cluster = static_cast<int>(P.sp.cluster);
+  out->cluster = 0;
   return MAG_OK;
 }
 
@@ -798,8 +882,11 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
     const Plan& P = e->plan;
     const SearchGeometry sg = geometry(e, len, 1);
     const uint64_t slices = sg.num_slices;
-    const uint64_t slice_bytes =
-        sg.slice_samples * (P.sp.verify_all || P.sp.overlapping ? 1 : P.sp.q * P.sp.k);
+    // bytes past a slice's last sample that its scan may read: the staged
+    // halo, and verification compares of whole patterns (global reads up to
+    // a + maxlen + 32, a up to a sample width past the slice end)
+    const uint64_t reach = static_cast<uint64_t>(P.back) + e->pd.maxlen +
+                           2 * std::max<uint64_t>(16, sg.bps) + 96;
     const uint64_t chunk = std::max<uint64_t>(uint64_t(64) << 20, (len + 31) / 32);
     std::vector<SliceRange> ranges;
     uint64_t copied = 0, slices_done = 0;
@@ -816,9 +903,7 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
       }
       MAG_CUDA(cudaEventRecord(w->chunk_ev[ci], w->copy_stream));
       // slices whose bytes (plus the pattern reach) have fully arrived
-      const uint64_t reach = P.back + 64;
-      uint64_t ready = copied == len ? slices : (copied > reach ? (copied - reach) / slice_bytes : 0);
-      ready = std::min(ready, slices);
+      const uint64_t ready = copied == len ? slices : (copied > reach ? slices_ending_by(sg, copied - reach) : 0);
       ranges.push_back(SliceRange{slices_done, ready, w->chunk_ev[ci]});
       slices_done = std::max(slices_done, ready);
       ++ci;

@@ -206,7 +206,7 @@ namespace {
 constexpr uint32_t kChunkTarget = 1536;   // gram bytes per ring slot
 constexpr uint32_t kSliceTarget = 32768;  // text bytes per warp work item
 constexpr uint32_t kDefaultRing = 2;
-constexpr uint32_t kDefaultWarps = 16;
+constexpr uint32_t kDefaultWarps = kMaxWarps - 1;  // scanning warps; the CTA adds its gather warp
 
 unsigned pow2ceil_log2(unsigned x) {
   unsigned l = 0;
@@ -246,7 +246,6 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
                  kCostProbeBit = 3,  // per extra probe bit of a multi-probe gram
                  kCostPf = 15,       // shared-memory prefilter test
                  kCostDirectHit = 120,  // direct kernel: a filter hit issues one L2 screen load
-                 kCostClusterLookup = 25,  // direct: DSMEM table lookup, per byte (W = 16), measured
                  kCostRollPos = 24,   // roll kernel: roll + one Bloom word per position
                  kCostRollProbe = 1.5,  // each Bloom probe
                  kCostRollBatch = 6,  // a verification batch (expansion, keys, slot loads) per 64 bytes of lane work
@@ -306,7 +305,7 @@ void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
       align16(chunk_bytes + static_cast<uint64_t>(ov) * bps + qm1 + extra + P->back + 15));
   P->slot_bytes = P->full_bytes + 32;
   P->ring = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultRing;
-  P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kDefaultWarps;
+  P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kDefaultWarps;
 }
 
 size_t fixed_smem(const Plan& P) {
@@ -442,7 +441,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       uint32_t chunk = kChunkTarget;
       int direct = 0;
       int roll = 0;
-      uint32_t roll_words = 0, halo = 0, ddepth = 0, cluster = 0, warps = 0;
+      uint32_t roll_words = 0, halo = 0, ddepth = 0, warps = 0;
       uint32_t blocks = 0;
       bool va = true;
       int og = 0;
@@ -558,12 +557,11 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
             (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
-      // W = 16 plans run 15 warps: measured cfg4 13/14/15/16 warps = 2,551/
-      // 2,604/2,686/1,934 GB/s (a 16th warp leaves L1 ~17 KB; the screen and
-      // bucket loads go through it) and cfg2 15 vs 16 = 4,802 vs 4,689 GB/s.
-      // W = 8 plans (cfg3) keep 16: 3,110 vs 2,968 GB/s at 15.
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, q == 8 ? 16u : kDirectMaxWarps)
-                                          : (q == 16 ? 15u : 16u);
+      // 15 scanning warps + the CTA's gather warp.  Round 1 (no gather warp)
+      // measured W = 16 at 13/14/15/16 warps: cfg4 2,551/2,604/2,686/1,934
+      // GB/s (a 16th scanning warp leaves L1 ~17 KB for the screen and bucket
+      // loads), cfg2 15 vs 16 = 4,802 vs 4,689 GB/s.
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)
@@ -617,37 +615,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.blocks = H > 1 ? blocks : 0;
           best.tb = H > 1 ? 0 : tb1;
           best.ddepth = H > 1 ? static_cast<uint32_t>(rq.stages) : depth1;
-          best.cluster = 0;
-          best.warps = warps;
-        }
-      }
-      // single-probe table spread over a cluster of 8 CTAs (8x the bits,
-      // read through distributed shared memory).  Opt-in only (cluster = 8):
-      // measured on B200 a remote lookup per sample caps the scan near
-      // 1.3 TB/s (cfg2 1,348 vs 4,154 GB/s; cfg4 1,216 vs 2,261 GB/s even
-      // with 4.6x fewer candidates), far below the local 2^20-bit table
-      if (q == 16 && depth1 == 2 && (rq.probes <= 1) && warps <= 16 && rq.cluster == 8) {
-        const unsigned tbc = tb1 + 3;
-        const double fill = 1.0 - std::exp(-distinct / std::ldexp(1.0, static_cast<int>(tbc)));
-        const double cpb = (exact + (1.0 - exact) * fill) / q;
-        const double cost = kStagedScale * (kCostSample + 2 * kCostProbeBit) / q + kCostClusterLookup +
-                            cpb * (kCostDirectHit + 0.008 * (kCostCand + kCostProbe + hits * kCostCompare));
-        if ((rq.cluster == 8 || cost < best.cost * 0.999) && tbc <= 26) {
-          best.cost = cost;
-          best.q = q;
-          best.k = 1;
-          best.mp = 1;
-          best.H = 1;
-          best.pf = 0;
-          best.chunk = kChunkTarget;
-          best.va = false;
-          best.cpb = cpb;
-          best.direct = 1;
-          best.og = 0;
-          best.blocks = 0;
-          best.tb = tbc;
-          best.ddepth = depth1;
-          best.cluster = 8;
           best.warps = warps;
         }
       }
@@ -663,7 +630,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           q = c;
           break;
         }
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
       const uint32_t v4 = (32 + q - 1 + 15) / 16;
       const uint32_t halo = static_cast<uint32_t>(
           align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
@@ -722,7 +689,6 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.blocks = best.H > 1 ? (best.direct ? best.blocks : static_cast<uint32_t>((1ull << best.tb) / 64)) : 0;
       sp.direct = best.direct;
       sp.ddepth = best.ddepth;
-      sp.cluster = best.cluster;
       best_warps = best.warps;
       sp.roll = best.roll;
       best_halo = best.halo;
@@ -774,7 +740,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->slice_samples = static_cast<uint64_t>(kRollStep) * 16;
     P->back = best_halo;
     P->ring = kRollDepth;
-    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : 16;
+    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
   }
 
   // ---- shared-memory placement
@@ -792,7 +758,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.table_in_smem = sp.verify_all ? 0 : 1;
     if (sp.direct)
       P->nwarps = best_warps ? best_warps
-                             : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, sp.q == 8 ? 16u : kDirectMaxWarps) : 16u);
+                             : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1);
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;

@@ -148,8 +148,7 @@ struct ScanPlan {
   uint32_t table_bits;    // hashed: log2(entries)
   uint32_t probes;        // hashed, m' = k = 1: entries probed per gram (1..kMaxProbes)
   uint32_t blocks;        // probes >= 2: 64-entry blocks in the table
-  int direct;             // q = 16 stream kernel (register prefetch, no staging)
-  uint32_t cluster;       // direct: CTAs per cluster sharing the table through DSMEM (0/1 = none)
+  int direct;             // aligned-sample stream kernel (W = q = 16 or 8)
   uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
@@ -172,7 +171,8 @@ struct ScanPlan {
   // Window keys are screened by an L2-resident bitmap of 2^l2_bits bits
   // (bit = screen_bit(key)) before any bucket walk; 0 = no bitmap.
   uint32_t l2_bits;
-  // diagnostics only (MAG_B200_DIAG env): 1 = skip candidate verification
+  // diagnostics only (builds with -DMAG_B200_DIAGNOSTICS read MAG_B200_DIAG;
+  // product builds always pass 0): bits skip stages for profiling
   int diag;
   uint32_t pf_bits;       // prefilter bitmap has 2^pf_bits bits (smem)
   uint32_t bucket_bits;   // 2^bucket_bits buckets (global)
@@ -182,7 +182,7 @@ struct ScanPlan {
 
 // ---- shared-memory layout of the scan kernel (host computes the size,
 // device carves it; one definition for both).
-constexpr int kMaxWarps = 16;   // warps per CTA (launch bound: 512 threads)
+constexpr int kMaxWarps = 16;   // warps per CTA, gather warp included (launch bound: 512 threads)
 constexpr int kQueueCap = 64;   // candidate windows queued per warp (per chunk)
 constexpr int kProbeCap = 128;  // window keys awaiting the L2 screen (per slice)
 constexpr int kHitWords = 32;   // per-chunk hit bitmap (chunks of <= 1024 samples, k = 1)
@@ -207,18 +207,16 @@ struct SmemLayout {
 // Direct (q = 16) kernel: resident table, per-warp probe queue, and a ring
 // of kDirectDepth 1 KiB step buffers (+ mbarriers) per warp.
 constexpr int kDirectDepth = 4;
-constexpr int kDirectMaxWarps = 24;  // direct kernel: up to 768 threads (3-deep rings past 16 warps)
-// Ring depth of the direct kernel: the plan's (2..4), 3 past 16 warps.
-MAG_HD int direct_depth(const ScanPlan& p, uint32_t nwarps) {
-  return nwarps > 16 ? 3 : (p.ddepth >= 2 && p.ddepth <= 4 ? static_cast<int>(p.ddepth) : kDirectDepth);
+// Ring depth of the direct kernel: the plan's (2..4).
+MAG_HD int direct_depth(const ScanPlan& p, uint32_t /*nwarps*/) {
+  return p.ddepth >= 2 && p.ddepth <= 4 ? static_cast<int>(p.ddepth) : kDirectDepth;
 }
-constexpr int kDirectStep = 128;  // samples per W=16 step before round 1's 2.5 KiB steps
 // Text bytes per direct-kernel step: 256 16-byte samples or 256 8-byte
 // samples (8 per lane either way).
 MAG_HD uint32_t direct_step_bytes(uint32_t q) { return q == 8 ? 2048u : 4096u; }
 constexpr int kDirectProbeCap = 64;  // direct kernel: screened window keys queued per warp
 MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
-  return align16(p.table_bytes / (p.cluster > 1 ? p.cluster : 1)) + align16(size_t(nwarps) * kDirectProbeCap * 8) +
+  return align16(p.table_bytes) + align16(size_t(nwarps) * kDirectProbeCap * 8) +
          size_t(nwarps) * direct_depth(p, nwarps) * (direct_step_bytes(p.q) + 16 + 8) + 64;
 }
 

@@ -1,0 +1,81 @@
+// Kernel-family dispatch, the SMAG prepare kernel and launch bookkeeping.
+#include <atomic>
+#include <mutex>
+#include <set>
+#include <utility>
+
+#include "scan_launch.h"
+
+namespace magb {
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+
+// SMAG prepare (encode_text qgram.cpp:29-37) on the device.
+__global__ void mag_encode_kernel(const ScanPlan P, const uint8_t* __restrict__ text, uint64_t nq,
+                                  const uint8_t* __restrict__ map, uint32_t* __restrict__ codes) {
+  __shared__ uint8_t smap[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) smap[i] = map ? map[i] : 0;
+  __syncthreads();
+  const uint32_t q = P.q;
+  for (uint64_t u = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; u < nq; u += (uint64_t)gridDim.x * blockDim.x) {
+    const uint8_t* g = text + u * q;
+    uint32_t v;
+    if (P.gram_mode == kGramExact) {
+      v = smap[g[q - 1]];
+      for (int i = static_cast<int>(q) - 2; i >= 0; --i) v = v * P.sigma_prime + smap[g[i]];
+    } else {
+      uint32_t x[4] = {0, 0, 0, 0};
+      for (uint32_t i = 0; i < q; ++i) x[i >> 2] |= static_cast<uint32_t>(g[i]) << (8 * (i & 3));
+      v = gram_slot(hash_gram_words(x[0], x[1], x[2], x[3]), P.table_bits);
+    }
+    codes[u] = v;
+  }
+}
+
+}  // namespace
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+unsigned long long kernel_launch_count() { return g_launches.load(); }
+
+cudaError_t allow_max_smem(const void* kernel, size_t need) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count({kernel, dev})) return cudaSuccess;
+  int optin = 0;
+  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  if (need > static_cast<size_t>(optin)) return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+  if (e != cudaSuccess) return e;
+  done.insert({kernel, dev});
+  return cudaSuccess;
+}
+
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
+  if (a.plan.direct) return launch_direct(a, stream, grid);
+  if (a.plan.roll) return launch_roll(a, stream, grid);
+  if (a.plan.smag) return launch_staged_codes(a, stream, grid);
+  if (a.plan.gram_mode == kGramHashed) return launch_staged_hashed(a, stream, grid);
+  return launch_staged_exact(a, stream, grid);
+}
+
+cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n, const uint8_t* map,
+                          uint32_t* codes, cudaStream_t stream) {
+  const uint64_t nq = n / plan.q;
+  if (nq == 0) return cudaSuccess;
+  const int threads = 256;
+  uint64_t blocks = (nq + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  (void)cudaGetLastError();
+  mag_encode_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(plan, text, nq, map, codes);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace magb

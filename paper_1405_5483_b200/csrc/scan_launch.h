@@ -1,4 +1,4 @@
-// Host-side view of the device search kernels (scan_kernels.cu).
+// Host-side view of the device search kernels (scan_*.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,11 +10,22 @@ namespace magb {
 // Everything one scan launch needs.  Device pointers only.
 //
 // Work decomposition: the filter's samples t in [0, samples) are cut into
-// slices of slice_samples; a slice is owned by one warp (dynamic ticket) and
-// produces the matches of exactly the candidate windows its samples raise,
-// in (offset, pattern) order, into staging + slice * slice_cap.  A slice is
-// streamed through the warp's ring of shared-memory slots in chunks of
-// chunk_samples samples (TMA bulk copies, one mbarrier per slot).
+// slices — big_slices slices of slice_samples, then tail slices of
+// tail_samples (smaller, so the last wave of the grid ends together).  A
+// slice is owned by one warp (dynamic ticket) and produces the matches of
+// exactly the candidate windows its samples raise, in (offset, pattern)
+// order, into staging + slice * slice_cap.  A slice is streamed through the
+// warp's ring of shared-memory slots in chunks of chunk_samples samples (TMA
+// bulk copies, one mbarrier per slot).
+//
+// Ordered gather (no second kernel): at the end of a slice its owner
+// publishes (epoch << 32 | count) in slice_state[slice].  The last warp of
+// every CTA is a gather warp: any gather warp that finds published slices
+// right above the watermark (counters[0]) computes their inclusive prefix
+// counts into incl[], claims them with one CAS on the watermark and copies
+// their staged matches to out[prefix..].  The last warp to leave the final
+// launch of a search writes the counters to host_ctr (mapped pinned host
+// memory) and zeroes the next search's control words.
 struct ScanArgs {
   ScanPlan plan;
   const uint8_t* text;          // 16-byte aligned
@@ -33,38 +44,52 @@ struct ScanArgs {
   uint32_t vmask;
   uint32_t zero;                // always 0; opaque to the compiler (orders slot reads before TMA refills)
   uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping, n verify-all
-  uint64_t slice_samples;       // multiple of chunk_samples
+  uint64_t slice_samples;       // big slices: multiple of chunk_samples
+  uint64_t big_slices;          // slices [0, big_slices) are big, the rest tail slices
+  uint64_t tail_samples;        // tail slices: multiple of chunk_samples, <= slice_samples
   uint32_t chunk_samples;       // samples per chunk (iterations * advance)
   uint32_t back;                // staged bytes after the last gram (pattern reach)
   uint32_t full_bytes;          // staged bytes of an interior chunk (multiple of 16)
   uint32_t slot_bytes;          // one ring slot (multiple of 16, >= full_bytes + 32)
   uint32_t ring;                // slots per warp
-  uint32_t nwarps;              // warps per CTA
+  uint32_t nwarps;              // scanning warps per CTA (the CTA has one more: the gather warp)
   uint64_t slice_begin, slice_end;  // slices of this launch
   uint64_t num_slices;
   uint64_t* staging;            // num_slices * slice_cap packed matches
-  uint32_t slice_cap;
-  uint32_t* slice_count;        // exact per-slice counts (even past slice_cap)
-  unsigned long long* counters; // [1] candidates [2] matches [3] max slice count
+  uint32_t slice_cap;           // multiple of 16 (slices never share a 128-byte line)
+  uint32_t epoch;               // this search's tag in slice_state
+  uint64_t* slice_state;        // per slice: epoch << 32 | exact match count (even past slice_cap)
+  uint64_t* incl;               // per slice: inclusive prefix of counts (valid below the watermark)
+  uint64_t* out;                // sorted output
+  uint64_t out_cap;
+  unsigned long long* counters; // [0] watermark [1] candidates [2] matches [3] max slice count
   unsigned long long* ticket;   // slice ticket of this launch (zeroed)
-  unsigned long long* reset;    // compaction zeroes reset[0..reset_words) (next search's counters)
+  unsigned long long* exits;    // warps of this launch that have left (zeroed)
+  uint32_t launch_warps;        // warps of this launch (grid * (nwarps + 1))
+  uint32_t final_launch;        // 1: the search's last launch publishes the counters
+  unsigned long long* host_ctr; // mapped pinned host copy of counters [1..3]
+  unsigned long long* reset;    // zeroed by the final launch's last warp (next search's control words)
   uint32_t reset_words;
 };
+
+// Slice geometry (host and device).
+MAG_HD uint64_t slice_t0(const ScanArgs& a, uint64_t x) {
+  return x < a.big_slices ? x * a.slice_samples
+                          : a.big_slices * a.slice_samples + (x - a.big_slices) * a.tail_samples;
+}
+MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
+  const uint64_t t = slice_t0(a, x) + (x < a.big_slices ? a.slice_samples : a.tail_samples);
+  return t < a.samples ? t : a.samples;
+}
 
 struct LaunchShape {
   size_t smem_bytes;
   unsigned threads;
 };
 
-LaunchShape scan_shape(const ScanArgs& a);
-
-// Enqueues the fused filter + verify kernel (persistent, `grid` CTAs).
+// Enqueues the fused filter + verify + ordered-gather kernel (persistent,
+// `grid` CTAs).
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid);
-
-// Gathers the staged slices into the sorted output (out[0..total)) and
-// writes counters[2] (total) and counters[3] (largest slice count).
-cudaError_t launch_compact(const ScanArgs& a, uint64_t* out, uint64_t out_cap, cudaStream_t stream,
-                           int grid);
 
 // SMAG prepare: codes[u] = mask index of gram u, for u < n/q.
 cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,
@@ -72,5 +97,16 @@ cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,
 
 // Number of kernels this library has enqueued (process lifetime).
 unsigned long long kernel_launch_count();
+
+// ---- internal: per-family launchers (scan_*.cu)
+cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid);
+cudaError_t launch_roll(const ScanArgs& a, cudaStream_t stream, int grid);
+cudaError_t launch_staged_exact(const ScanArgs& a, cudaStream_t stream, int grid);
+cudaError_t launch_staged_hashed(const ScanArgs& a, cudaStream_t stream, int grid);
+cudaError_t launch_staged_codes(const ScanArgs& a, cudaStream_t stream, int grid);
+void count_launch();
+// Raises a kernel's dynamic shared-memory limit to the device's opt-in
+// maximum, once per (kernel, device); thread-safe.
+cudaError_t allow_max_smem(const void* kernel, size_t need);
 
 }  // namespace magb

@@ -389,14 +389,13 @@ def test_concurrent_searches_one_engine(mag, ref):
         assert got == want, kernel
 
 
-@pytest.mark.parametrize("q,cluster", [(8, 1), (16, 1), (16, 8)])
-def test_direct_kernel(mag, ref, port, q, cluster):
-    """The aligned-sample kernel (forced), both sample widths, and the table
-    shared by 8-CTA clusters through distributed shared memory: texts of every
-    length class around its 128-sample step (odd 8-byte sample counts
-    included), m = 2q-1 (the shortest admissible) up to patterns longer than
-    any staged halo, duplicates, dense plants, misaligned device text; the
-    candidate counter equals the restated hashed machine's."""
+@pytest.mark.parametrize("q,probes", [(8, 1), (16, 1), (16, 3)])
+def test_direct_kernel(mag, ref, port, q, probes):
+    """The aligned-sample kernel (forced), both sample widths, single- and
+    multi-probe tables: texts of every length class around its step (odd
+    8-byte sample counts included), m = 2q-1 (the shortest admissible) up to
+    patterns longer than any staged halo, duplicates, dense plants, misaligned
+    device text; the candidate counter equals the restated hashed machine's."""
     rng = np.random.default_rng(50 + q)
     step = 128 * q
     sizes = [0, 5, q, 2 * q - 1, step - 8, step, step + 8, step + 24, 3 * step + 8, 2048 * q + 40, 250_000]
@@ -421,9 +420,9 @@ def test_direct_kernel(mag, ref, port, q, cluster):
             if len(p) < n:
                 s0 = int(rng.integers(0, n - len(p) + 1))
                 text[s0:s0 + len(p)] = np.frombuffer(p, dtype=np.uint8)
-        e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED, cluster=cluster)
+        e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED, probes=probes)
         pl = e.plan()
-        assert pl["direct"] == 1 and pl["q"] == q and pl["cluster"] == (8 if cluster == 8 else 0), pl
+        assert pl["direct"] == 1 and pl["q"] == q and pl["probes"] == probes, pl
         got, met = gpu_pairs(e, text)
         assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
         P = port.params(variant=0, gram_mode=1, q=q, k=1, table_bits=pl["table_bits"], word_bits=1,
@@ -435,3 +434,78 @@ def test_direct_kernel(mag, ref, port, q, cluster):
             d = torch.from_numpy(text).cuda()
             pd = e.prepare_device(d.data_ptr() + 3, n - 3, keep=d)
             assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[3:], pats))
+
+
+def _boundary_patterns(rng, text, bounds, lengths):
+    """Patterns copied from the text so that their occurrences straddle every
+    boundary in `bounds` (start = b - x for x from 1 to len - 1)."""
+    pats = []
+    for b in bounds:
+        for L in lengths:
+            for x in (1, 17, L // 2, L - 1, int(rng.integers(1, L))):
+                s0 = b - x
+                if 0 <= s0 and s0 + L <= text.size:
+                    pats.append(text[s0:s0 + L].tobytes())
+    return pats
+
+
+@pytest.mark.parametrize("kernel", ["direct", "staged", "roll"])
+def test_mag_search_copy_chunk_boundaries(mag, ref, kernel):
+    """mag_search (pinned-copy pipeline) on a 200 MiB text (copy chunks of
+    64 MiB): occurrences of 0.6-4 KiB patterns straddle every copy-chunk
+    boundary, the workspace is pre-dirtied by a search of a different text,
+    and the result equals the reference Aho-Corasick (oracles.cpp:78-95).
+    Round 1 released a slice once its staging halo had arrived, not its
+    longest pattern's reach (host_engine.cpp mag_search)."""
+    rng = np.random.default_rng(77)
+    n = 200 << 20
+    text = (rng.integers(0, 4, n, dtype=np.uint8) + 65).astype(np.uint8)
+    chunk = 64 << 20
+    bounds = list(range(chunk, n, chunk))
+    if kernel == "roll":
+        pats = _boundary_patterns(rng, text, bounds, [600, 700])
+        pats += [(rng.integers(0, 4, 12) + 65).astype(np.uint8).tobytes() for _ in range(300)]
+        pats += [text[s:s + 12].tobytes() for s in rng.integers(0, n - 12, 300)]
+    else:
+        pats = _boundary_patterns(rng, text, bounds, [1536, 2500, 4096])
+        pats += [text[s:s + 1600].tobytes() for s in rng.integers(0, n - 1600, 20)]
+    e = mag.Engine(pats, scan_kernel=kernel)
+    pl = e.plan()
+    assert (pl["direct"], pl["roll"]) == {"direct": (1, 0), "staged": (0, 0), "roll": (0, 1)}[kernel], pl
+    other = (rng.integers(0, 4, n, dtype=np.uint8) + 65).astype(np.uint8)
+    e.search(other).close()  # leaves stale text in the workspace's device buffer
+    got = e.search(text).arrays()
+    want = ref.ac(text, pats, threads=8)
+    assert got[0].size == want[0].size, (kernel, got[0].size, want[0].size, pl)
+    assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), (kernel, pl)
+
+
+@pytest.mark.parametrize("q", [8, 16])
+def test_text_beyond_2p32_samples(mag, q):
+    """The direct kernel past 2^32 samples (W = 8: a 32 GiB text; W = 16:
+    64 GiB) in device memory: random 64-byte patterns planted before, at and
+    after the 2^32-sample offset are found exactly there (the sample cursor
+    and offsets are 64-bit; random 64-mers occur by chance with p ~ 4^-64)."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    n = (q << 32) + (3 << 20)
+    if free < n + (8 << 30):
+        pytest.skip(f"needs {n >> 30} GiB of free device memory")
+    rng = np.random.default_rng(64 + q)
+    pats = [(rng.integers(0, 4, 64) + 65).astype(np.uint8).tobytes() for _ in range(8)]
+    d = torch.randint(0, 4, (n,), dtype=torch.uint8, device="cuda")
+    d.add_(65)
+    edge = q << 32
+    offs = [5, edge - 4096, edge - 40, edge - 3, edge, edge + 8 * 12345 + 3, n - 64 - 7, n - 64]
+    want = []
+    for i, o in enumerate(offs):
+        p = i % len(pats)
+        d[o:o + 64] = torch.frombuffer(bytearray(pats[p]), dtype=torch.uint8).cuda()
+        want.append((o, p))
+    e = mag.Engine(pats, scan_kernel="direct", q=q, gram_mode=mag.GRAM_HASHED)
+    assert e.plan()["direct"] == 1 and e.plan()["q"] == q
+    prep = e.prepare_device(d.data_ptr(), n, keep=d)
+    got = e.search_prepared(prep).pairs()
+    assert got == sorted(want), (got, sorted(want))
+    del prep, d
+    torch.cuda.empty_cache()
