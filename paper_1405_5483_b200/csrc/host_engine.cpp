@@ -56,7 +56,7 @@ cudaError_t upload(const std::vector<T>& v, T** out) {
 // Per-search device scratch, pooled per engine.  `done` orders reuse on the
 // device (a later search waits for it with cudaStreamWaitEvent).
 struct Workspace {
-  // two halves of counters[8] | tickets[kMaxLaunch] | exits[kMaxLaunch]: a
+  // two halves of kCtrWords control words (scan_launch.h): a
   // search uses half `parity` and the last warp of its final launch zeroes
   // the other half for the next search on this workspace (no memset launch
   // per search).  `dirty`: a search failed half-way; both halves are
@@ -71,7 +71,7 @@ struct Workspace {
   uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
   uint64_t* out = nullptr;             // sorted matches (same capacity)
   size_t out_cap = 0;
-  unsigned long long* h_ctr = nullptr;  // mapped pinned counters[8], written by the kernel
+  unsigned long long* h_ctr = nullptr;  // mapped pinned [1] candidates [2] matches [3] max, written by the kernel
   unsigned long long* d_hctr = nullptr; // its device alias
   uint8_t* text = nullptr;              // device copy of host text (mag_search)
   size_t text_cap = 0;
@@ -97,7 +97,7 @@ struct Workspace {
   }
 };
 
-constexpr size_t kMaxLaunch = 64;
+constexpr size_t kMaxLaunch = kMaxLaunches;
 
 // Optional device timing of the scan kernel launches (bench/profiling only):
 // CUDA events around every launch_scan, read back by mag_scan_timer_read.
@@ -234,7 +234,7 @@ void release(const mag_engine* e, std::unique_ptr<Workspace> w) {
 }
 
 constexpr size_t kCounters = 8;
-constexpr size_t kCtrlWords = kCounters + 2 * kMaxLaunch;
+constexpr size_t kCtrlWords = kCtrWords;
 
 struct SearchGeometry {
   uint64_t samples, slice_samples, tail_samples, big_slices, num_slices, slice_cap;
@@ -431,8 +431,9 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     if (li >= kMaxLaunch) return fail(MAG_ERR_INTERNAL, "too many scan launches for one search");
     a.slice_begin = begin;
     a.slice_end = end;
-    a.ticket = counters + kCounters + li;
-    a.exits = counters + kCounters + kMaxLaunch + li;
+    a.ticket = counters + kCtrLaunch + kCtrPerLaunch * li;
+    a.exits = a.ticket + 16;
+    a.copy_cursor = a.ticket + 32;
     ++li;
     const uint64_t ctas = std::max<uint64_t>(1, (end - begin + P.nwarps - 1) / P.nwarps);
     const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));

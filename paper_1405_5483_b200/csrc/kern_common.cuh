@@ -68,6 +68,8 @@ __device__ __forceinline__ uint64_t ld_gpu(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Release/acquire fence at GPU scope (lighter than __threadfence's fence.sc).
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -194,11 +196,11 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
 // The largest slice count (staging overflow check, learned density) is a
 // fire-and-forget reduction.
 __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
+  fence_gpu();  // every lane's staged matches before the state
   __syncwarp();
   if (lane == 0) {
-    __threadfence();
     st_gpu(A.slice_state + slice, (static_cast<uint64_t>(A.epoch) << 32) | count);
-    if (count) atomicMax(A.counters + 3, static_cast<unsigned long long>(count));
+    if (count) atomicMax(A.counters + kCtrMax, static_cast<unsigned long long>(count));
   }
   __syncwarp();
 }
@@ -210,80 +212,146 @@ __device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long 
   for (int o = 16; o; o >>= 1) cands += __shfl_xor_sync(kFull, cands, o);
   unsigned long long old = 0;
   if (lane == 0) {
-    if (cands) atomicAdd(A.counters + 1, cands);
-    __threadfence();
+    if (cands) atomicAdd(A.counters + kCtrCands, cands);
+    fence_gpu();
     old = atomicAdd(A.exits, 1ull);
   }
   old = __shfl_sync(kFull, old, 0);
   if (old + 1 != A.launch_warps || !A.final_launch) return;
-  __threadfence();
+  fence_gpu();
   if (lane < 3) {
-    const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + 1 + lane);
+    const unsigned src = lane == 0 ? kCtrCands : (lane == 1 ? kCtrTotal : kCtrMax);
+    const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + src);
     reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[1 + lane] = v;
   }
   for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
   __threadfence_system();
 }
 
-// The gather warp: advance the watermark over published slices (inclusive
-// prefix counts + one CAS), copy the claimed slices' staged matches to their
-// final place, until every slice of this launch is below the watermark.
-// Progress only depends on slices already claimed by running warps, so it
-// cannot deadlock on CTAs that are not resident.
-__device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
+// Watermark advance (one gather warp at a time, under the advance lock): up to
+// 32 x 32 published slices right above W get their inclusive prefix counts
+// in incl[]; the new watermark is stored after them.  Returns the new W.
+// One round trip for the states, one for the stores: ~1000 slices per
+// advance keeps pace with the scanning warps (~250 slices per microsecond).
+__device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_t W, int lane) {
+  constexpr int kRounds = 32;
   const uint64_t epoch = A.epoch;
-  uint64_t W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters));
-  __threadfence();
-  uint32_t idle = 0;
-  while (W < A.slice_end) {
-    const uint64_t x = W + lane;
-    uint64_t st = 0;
-    if (x < A.slice_end) st = ld_gpu(A.slice_state + x);
-    const bool done = x < A.slice_end && (st >> 32) == epoch;
+  uint64_t st[kRounds];
+#pragma unroll
+  for (int i = 0; i < kRounds; ++i) {
+    const uint64_t x = W + 32ull * i + lane;
+    st[i] = x < A.slice_end ? ld_gpu(A.slice_state + x) : 0ull;
+  }
+  unsigned long long base = W == 0 ? 0ull : ld_gpu(A.incl + W - 1);
+  fence_gpu();  // the observed states' staged matches are visible to the copiers
+  uint64_t j = 0;
+  bool stop = false;
+#pragma unroll
+  for (int i = 0; i < kRounds; ++i) {
+    if (stop) break;  // warp-uniform
+    const bool done = (st[i] >> 32) == epoch && W + 32ull * i + lane < A.slice_end;
     const unsigned nd = __ballot_sync(kFull, !done);
-    const uint32_t j = nd ? static_cast<uint32_t>(__ffs(nd) - 1) : 32u;  // leading published slices
-    if (j == 0) {
-      __nanosleep(idle < 4 ? 200 : 800);
-      ++idle;
-      W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters));
-      __threadfence();
-      continue;
-    }
-    idle = 0;
-    __threadfence();  // the states above were observed: their staging is visible
-    const uint64_t base = W == 0 ? 0ull : ld_gpu(A.incl + W - 1);
-    const uint32_t cnt = static_cast<uint32_t>(lane < static_cast<int>(j) ? st : 0ull);
-    // inclusive prefix of the j counts (64-bit)
+    const uint32_t lead = nd ? static_cast<uint32_t>(__ffs(nd) - 1) : 32u;
+    const uint32_t cnt = lane < static_cast<int>(lead) ? static_cast<uint32_t>(st[i]) : 0u;
     unsigned long long v = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const unsigned long long y = __shfl_up_sync(kFull, v, o);
       if (lane >= o) v += y;
     }
-    if (lane < static_cast<int>(j)) st_gpu(A.incl + x, base + v);
-    const unsigned long long last = __shfl_sync(kFull, base + v, j - 1);
-    if (W + j == A.num_slices && lane == 0) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + 2, last);
-    __threadfence();
-    unsigned long long old = 0;
-    if (lane == 0) old = atomicCAS(A.counters, static_cast<unsigned long long>(W), W + j);
-    old = __shfl_sync(kFull, old, 0);
-    if (old != W) {  // another gather warp advanced first
-      W = old;
-      __threadfence();
-      continue;
+    if (lane < static_cast<int>(lead)) st_gpu(A.incl + W + 32ull * i + lane, base + v);
+    base += __shfl_sync(kFull, v, 31);
+    j += lead;
+    stop = lead < 32;
+  }
+  if (j == 0) return W;
+  W += j;
+  fence_gpu();  // every lane's incl stores before the new watermark
+  __syncwarp();
+  if (lane == 0) {
+    if (W == A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, base);
+    fence_gpu();
+    st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrWatermark, W);
+  }
+  __syncwarp();
+  return W;
+}
+
+// Copy slices [c, c + 32) (all below the watermark) to their final place.
+__device__ __forceinline__ void copy_slices(const ScanArgs& A, uint64_t c, int lane) {
+  const uint64_t x = c + lane;
+  uint32_t cnt = 0;
+  unsigned long long end = 0;
+  if (x < A.slice_end) {
+    cnt = static_cast<uint32_t>(ld_gpu(A.slice_state + x));
+    end = ld_gpu(A.incl + x);
+  }
+  for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
+    const int s = __ffs(m) - 1;
+    const uint32_t n = __shfl_sync(kFull, cnt, s);
+    const unsigned long long dst = __shfl_sync(kFull, end, s) - n;
+    const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
+    const uint64_t* src = A.staging + (c + s) * A.slice_cap;
+    for (uint32_t i = lane; i < cc; i += 32)
+      if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
+  }
+}
+
+// The gather warp of every CTA.  Two jobs: advancing the watermark (any
+// gather warp that takes the advance lock), and copying: each gather warp
+// claims 32 slices at a time (a cursor per launch) and copies them once the
+// watermark has passed them.  Progress only depends on slices already claimed
+// by running scanning warps, so it cannot deadlock on CTAs that are not
+// resident.
+__device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
+  unsigned long long* lock = A.counters + kCtrLock;
+  uint64_t claim = ~0ull;
+  bool claims_done = false;
+  uint32_t idle = 0;
+  while (true) {
+    uint64_t W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
+    bool progress = false;
+    // the lock is only tried when the slice at the watermark is published
+    bool ready = false;
+    if (lane == 0 && W < A.slice_end) ready = (ld_gpu(A.slice_state + W) >> 32) == A.epoch;
+    if (__shfl_sync(kFull, ready, 0)) {
+      unsigned long long got = 1;
+      if (lane == 0) got = atomicCAS(lock, 0ull, 1ull);
+      got = __shfl_sync(kFull, got, 0);
+      if (got == 0) {
+        fence_gpu();
+        W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
+        const uint64_t W2 = advance_watermark(A, W, lane);
+        progress = W2 != W;
+        W = W2;
+        if (lane == 0) {
+          fence_gpu();
+          atomicExch(lock, 0ull);
+        }
+      }
     }
-    // claimed slices [W, W + j): copy their staged matches in order
-    const unsigned nz = __ballot_sync(kFull, cnt != 0);
-    for (unsigned m = nz; m; m &= m - 1) {
-      const int s = __ffs(m) - 1;
-      const uint32_t c = __shfl_sync(kFull, cnt, s);
-      const unsigned long long dst = __shfl_sync(kFull, base + v, s) - c;
-      const uint32_t cc = c < A.slice_cap ? c : A.slice_cap;
-      const uint64_t* src = A.staging + (W + s) * A.slice_cap;
-      for (uint32_t i = lane; i < cc; i += 32)
-        if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
+    if (!claims_done && claim == ~0ull) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(A.copy_cursor, 32ull);
+      c = __shfl_sync(kFull, c, 0) + A.slice_begin;
+      if (c >= A.slice_end)
+        claims_done = true;
+      else
+        claim = c;
     }
-    W += j;
+    if (claim != ~0ull && (claim + 32 <= W || W >= A.slice_end)) {
+      fence_gpu();
+      copy_slices(A, claim, lane);
+      claim = ~0ull;
+      progress = true;
+    }
+    if (claims_done && claim == ~0ull && W >= A.slice_end) break;
+    if (progress) {
+      idle = 0;
+    } else {
+      __nanosleep(idle < 8 ? 100 : 500);
+      ++idle;
+    }
   }
 }
 

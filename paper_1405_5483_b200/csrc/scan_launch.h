@@ -20,10 +20,11 @@ namespace magb {
 //
 // Ordered gather (no second kernel): at the end of a slice its owner
 // publishes (epoch << 32 | count) in slice_state[slice].  The last warp of
-// every CTA is a gather warp: any gather warp that finds published slices
-// right above the watermark (counters[0]) computes their inclusive prefix
-// counts into incl[], claims them with one CAS on the watermark and copies
-// their staged matches to out[prefix..].  The last warp to leave the final
+// every CTA is a gather warp: under a lock, one of them at a time advances
+// the watermark (counters[0]) over published slices, writing their
+// inclusive prefix counts into incl[]; every gather warp claims 32 slices at
+// a time below the watermark and copies their staged matches to
+// out[prefix..].  The last warp to leave the final
 // launch of a search writes the counters to host_ctr (mapped pinned host
 // memory) and zeroes the next search's control words.
 struct ScanArgs {
@@ -62,12 +63,13 @@ struct ScanArgs {
   uint64_t* incl;               // per slice: inclusive prefix of counts (valid below the watermark)
   uint64_t* out;                // sorted output
   uint64_t out_cap;
-  unsigned long long* counters; // [0] watermark [1] candidates [2] matches [3] max slice count
+  unsigned long long* counters; // control words (kCtr*)
   unsigned long long* ticket;   // slice ticket of this launch (zeroed)
   unsigned long long* exits;    // warps of this launch that have left (zeroed)
+  unsigned long long* copy_cursor;  // gather warps' copy claims of this launch (zeroed)
   uint32_t launch_warps;        // warps of this launch (grid * (nwarps + 1))
   uint32_t final_launch;        // 1: the search's last launch publishes the counters
-  unsigned long long* host_ctr; // mapped pinned host copy of counters [1..3]
+  unsigned long long* host_ctr; // mapped pinned host words: [1] candidates [2] matches [3] max slice count
   unsigned long long* reset;    // zeroed by the final launch's last warp (next search's control words)
   uint32_t reset_words;
 };
@@ -81,6 +83,19 @@ MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
   const uint64_t t = slice_t0(a, x) + (x < a.big_slices ? a.slice_samples : a.tail_samples);
   return t < a.samples ? t : a.samples;
 }
+
+// Control words of one search (a half of the workspace's ctrl array).
+// Each group has its own 128-byte line, so the scanning warps' ticket
+// atomics never share a line with the gather warps' polls.
+constexpr unsigned kCtrWatermark = 0;  // gather watermark
+constexpr unsigned kCtrTotal = 1;      // total matches (set when the watermark reaches the end)
+constexpr unsigned kCtrLock = 16;      // watermark-advance lock
+constexpr unsigned kCtrCands = 32;     // filter candidates
+constexpr unsigned kCtrMax = 48;       // largest slice count
+constexpr unsigned kCtrLaunch = 64;    // launch li: ticket at kCtrLaunch + kCtrPerLaunch * li, exits +16, copies +32
+constexpr unsigned kCtrPerLaunch = 48;
+constexpr unsigned kMaxLaunches = 64;
+constexpr unsigned kCtrWords = kCtrLaunch + kCtrPerLaunch * kMaxLaunches;
 
 struct LaunchShape {
   size_t smem_bytes;

@@ -209,41 +209,43 @@ struct RollScanner {
     return len <= 16 || equal_slot(sw, valid, a, pr, h.y, len);
   }
 
-  // Linear-probe run from the key's home slot (h, b already loaded): bit 31
-  // of a slot's len word says whether the next slot is occupied, so with a
-  // load factor <= 1/4 nearly every lookup is one L2 round trip.
-  __device__ uint32_t probe(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
-                            const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t* first,
-                            uint4 h, uint4 b) const {
-    uint32_t s = key & A.vmask, c = 0;
-    while (h.y != 0xffffffffu) {
+  // Rest of a linear-probe run after its home slot: bit 31 of a slot's len
+  // word says whether the next slot is occupied.  Adds to c (first pid kept
+  // in *first when c was 0), or writes from dst[idx + c].
+  __device__ __noinline__ uint32_t probe_rest(const uint32_t* sw, uint32_t valid, unsigned long long a, uint32_t pr,
+                                              const uint4& t, uint32_t key, uint64_t* dst, uint32_t idx, uint32_t c,
+                                              uint32_t* first) const {
+    uint32_t s = key & A.vmask;
+    while (true) {
+      s = (s + 1) & A.vmask;
+      const uint4 h = __ldg(A.vtab + 2 * s);
+      if (h.y == 0xffffffffu) break;
+      const uint4 b = __ldg(A.vtab + 2 * s + 1);
       if (slot_match(sw, valid, a, pr, t, key, h, b)) {
         if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, h.y);
         if (c == 0 && first) *first = h.y;
         ++c;
       }
       if (!(h.z >> 31)) break;
-      s = (s + 1) & A.vmask;
-      h = __ldg(A.vtab + 2 * s);
-      b = __ldg(A.vtab + 2 * s + 1);
     }
     return c;
   }
 
   // Expand and verify a step's hits in text order: run 0 (positions
-  // [32 l, 32 l + 32) of lane l) before run 1 ([1024 + 32 l, ...)).  Two
-  // candidates per lane per batch, so both verification-slot loads (one L2
-  // round trip each) are in flight together.
-  static constexpr int kVK = 3;
+  // [32 l, 32 l + 32) of lane l) before run 1 ([1024 + 32 l, ...)).  Each
+  // lane takes two candidates per batch (ranks base + lane, base + 32 +
+  // lane), both verification-slot loads in flight together; the home slot
+  // decides in straight-line code, the rare continued probe runs (and
+  // duplicate pattern keys, c > 1) take the slow paths.
   __device__ void verify_step(const uint32_t* sw, uint32_t valid, unsigned long long t, uint32_t h0,
                               uint32_t h1) {
     const uint32_t c0 = __popc(h0), c1 = __popc(h1);
-    const uint32_t e0 = warp_excl_scan(c0, lane), e1 = warp_excl_scan(c1, lane);
-    const uint32_t t0 = __shfl_sync(kFull, e0 + c0, 31), t1 = __shfl_sync(kFull, e1 + c1, 31);
-    const uint32_t total = t0 + t1;
+    const uint32_t packed = warp_excl_scan(c0 | (c1 << 16), lane);  // both prefix sums in one scan
+    const uint32_t e0 = packed & 0xffffu, e1 = packed >> 16;
+    const uint32_t tot = __shfl_sync(kFull, packed + (c0 | (c1 << 16)), 31);
+    const uint32_t t0 = tot & 0xffffu, total = t0 + (tot >> 16);
     cands32 += c0 + c1;
     if (A.plan.diag & 8) return;
-    const uint32_t packed = e0 | (e1 << 16);
     // Expansion: with at most kRollList hits each lane writes its own hit
     // positions at its prefix offsets (text order) into the warp's list;
     // denser steps rank-search the lane masks instead.
@@ -255,12 +257,13 @@ struct RollScanner {
       for (uint32_t m = h1; m; m &= m - 1) list[idx++] = static_cast<uint16_t>(1024 + 32 * lane + __ffs(m) - 1);
       __syncwarp();
     }
-    for (uint32_t base = 0; base < total; base += 32 * kVK) {
-      uint32_t pr[kVK], key[kVK], c[kVK], pid0[kVK];
-      uint4 tx[kVK], hq[kVK], bq[kVK];
-      bool live[kVK];
+    const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
+    for (uint32_t base = 0; base < total; base += 64) {
+      uint32_t pr[2], key[2], c[2], pid0[2];
+      uint4 tx[2], hq[2], bq[2];
+      bool live[2], more[2];
 #pragma unroll
-      for (int k = 0; k < kVK; ++k) {
+      for (int k = 0; k < 2; ++k) {
         const uint32_t rank = base + 32 * k + lane;
         live[k] = rank < total;
         if (listed) {
@@ -279,39 +282,58 @@ struct RollScanner {
           const uint32_t eo = (__shfl_sync(kFull, packed, o) >> sh) & 0xffffu;
           pr[k] = (r1 ? 1024u : 0u) + 32u * static_cast<uint32_t>(o) +
                   static_cast<uint32_t>(__fns(r1 ? m1 : m0, 0, static_cast<int>(rr - eo) + 1));
+          if (!live[k]) pr[k] = 0;
         }
-        if (!live[k]) pr[k] = 0;
         tx[k] = text16(sw, pr[k]);
         key[k] = key_of(tx[k]);
       }
-      // all slot loads after all expansions: a shuffle of candidate k+1
-      // would otherwise share a scoreboard with candidate k's loads and wait
-      // for them, serialising the round trips
+      // all slot loads after all expansions (a later shuffle would otherwise
+      // share a scoreboard with the earlier loads and serialise the trips)
 #pragma unroll
-      for (int k = 0; k < kVK; ++k) {
+      for (int k = 0; k < 2; ++k) {
         const uint32_t slot = key[k] & A.vmask;
-        const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
         hq[k] = live[k] ? __ldg(A.vtab + 2 * slot) : empty;
         bq[k] = live[k] ? __ldg(A.vtab + 2 * slot + 1) : empty;
       }
 #pragma unroll
-      for (int k = 0; k < kVK; ++k) {
-        pid0[k] = 0;
-        c[k] = probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], nullptr, 0, &pid0[k], hq[k], bq[k]);
+      for (int k = 0; k < 2; ++k) {
+        const bool occ = hq[k].y != 0xffffffffu;
+        c[k] = occ && slot_match(sw, valid, t + pr[k], pr[k], tx[k], key[k], hq[k], bq[k]) ? 1u : 0u;
+        pid0[k] = hq[k].y;
+        more[k] = occ && (hq[k].z >> 31);
+      }
+      if (__any_sync(kFull, more[0] || more[1])) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          if (more[k]) c[k] = probe_rest(sw, valid, t + pr[k], pr[k], tx[k], key[k], nullptr, 0, c[k], &pid0[k]);
       }
 #pragma unroll
-      for (int k = 0; k < kVK; ++k) {
-        if (!__any_sync(kFull, c[k] != 0)) continue;
+      for (int k = 0; k < 2; ++k) {
+        const unsigned one = __ballot_sync(kFull, c[k] == 1u);
+        if (!__any_sync(kFull, c[k] > 1u)) {  // one pattern per start (the common case)
+          if (c[k]) {
+            const uint32_t at = fill + __popc(one & ((1u << lane) - 1u));
+            if (at < A.slice_cap) out[at] = pack_match(t + pr[k], pid0[k]);
+          }
+          fill += __popc(one);
+          continue;
+        }
+        // duplicate pattern keys: every (start, pid) of the run, in order
         const uint32_t ex = warp_excl_scan(c[k], lane);
-        const uint32_t tot = __shfl_sync(kFull, ex + c[k], 31);
+        const uint32_t tc = __shfl_sync(kFull, ex + c[k], 31);
         if (c[k] == 1) {
           if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], pid0[k]);
         } else if (c[k] > 1) {
           const uint32_t slot = key[k] & A.vmask;
-          probe(sw, valid, t + pr[k], pr[k], tx[k], key[k], out, fill + ex, nullptr, __ldg(A.vtab + 2 * slot),
-                __ldg(A.vtab + 2 * slot + 1));
+          const uint4 h = __ldg(A.vtab + 2 * slot), b = __ldg(A.vtab + 2 * slot + 1);
+          uint32_t w = 0;
+          if (slot_match(sw, valid, t + pr[k], pr[k], tx[k], key[k], h, b)) {
+            if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], h.y);
+            w = 1;
+          }
+          if (h.z >> 31) probe_rest(sw, valid, t + pr[k], pr[k], tx[k], key[k], out, fill + ex, w, nullptr);
         }
-        fill += tot;
+        fill += tc;
       }
     }
   }
