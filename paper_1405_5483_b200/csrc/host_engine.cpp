@@ -272,8 +272,11 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
   const uint64_t unit = step_unit(P);
   g.tail_samples = std::min<uint64_t>(g.slice_samples,
                                       std::max<uint64_t>(unit, (g.slice_samples / 8 + unit - 1) / unit * unit));
-  const uint64_t tail = std::min<uint64_t>(g.samples / 2,
-                                           static_cast<uint64_t>(e->sm_count) * P.nwarps * g.slice_samples);
+  uint64_t tail = std::min<uint64_t>(g.samples / 2, static_cast<uint64_t>(e->sm_count) * P.nwarps * g.slice_samples);
+#ifdef MAG_B200_DIAGNOSTICS
+  if (const char* d = std::getenv("MAG_B200_DIAG"))
+    if (std::atoi(d) & 1024) tail = 0;  // profiling: uniform slices
+#endif
   g.big_slices = g.samples > tail ? (g.samples - tail) / g.slice_samples : 0;
   const uint64_t rest = g.samples - g.big_slices * g.slice_samples;
   g.num_slices = g.big_slices + (rest + g.tail_samples - 1) / g.tail_samples;

@@ -196,6 +196,7 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
 // The largest slice count (staging overflow check, learned density) is a
 // fire-and-forget reduction.
 __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
+  if (A.plan.diag & 512) return;  // diagnostics: no publication (no gather)
   fence_gpu();  // every lane's staged matches before the state
   __syncwarp();
   if (lane == 0) {
@@ -228,48 +229,59 @@ __device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long 
   __threadfence_system();
 }
 
-// Watermark advance (one gather warp at a time, under the advance lock): up to
-// 32 x 32 published slices right above W get their inclusive prefix counts
-// in incl[]; the new watermark is stored after them.  Returns the new W.
-// One round trip for the states, one for the stores: ~1000 slices per
-// advance keeps pace with the scanning warps (~250 slices per microsecond).
+// Watermark advance (one gather warp at a time, under the advance lock):
+// lane l takes the 32 slices W + 32 l ... W + 32 l + 31, so the published
+// run right above W (up to 1024 slices) is found and prefix-summed with
+// per-lane serial sums and one warp scan; the inclusive prefix counts go to
+// incl[] and the new watermark is stored after them.  About two round trips
+// per advance: far more than the ~250 slices per microsecond the scanning
+// warps publish.  Returns the new W.
 __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_t W, int lane) {
-  constexpr int kRounds = 32;
-  const uint64_t epoch = A.epoch;
-  uint64_t st[kRounds];
+  constexpr int kPer = 32;
+  const uint32_t epoch = A.epoch;
+  const uint64_t x0 = W + static_cast<uint64_t>(kPer) * lane;
+  uint64_t st[kPer];
 #pragma unroll
-  for (int i = 0; i < kRounds; ++i) {
-    const uint64_t x = W + 32ull * i + lane;
-    st[i] = x < A.slice_end ? ld_gpu(A.slice_state + x) : 0ull;
+  for (int i = 0; i < kPer; ++i) st[i] = x0 + i < A.slice_end ? ld_gpu(A.slice_state + x0 + i) : 0ull;
+  const unsigned long long base = W == 0 ? 0ull : ld_gpu(A.incl + W - 1);
+  // this lane's leading published slices and their count sum
+  int lead = kPer;
+  uint32_t sum = 0;
+#pragma unroll
+  for (int i = kPer - 1; i >= 0; --i)
+    if (static_cast<uint32_t>(st[i] >> 32) != epoch || x0 + i >= A.slice_end) lead = i;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i)
+    if (i < lead) sum += static_cast<uint32_t>(st[i]);
+  // the run ends in the first lane that is not fully published
+  const unsigned partial = __ballot_sync(kFull, lead < kPer);
+  const int stop = partial ? __ffs(partial) - 1 : 32;
+  if (lane > stop) {
+    lead = 0;
+    sum = 0;
   }
-  unsigned long long base = W == 0 ? 0ull : ld_gpu(A.incl + W - 1);
-  fence_gpu();  // the observed states' staged matches are visible to the copiers
-  uint64_t j = 0;
-  bool stop = false;
-#pragma unroll
-  for (int i = 0; i < kRounds; ++i) {
-    if (stop) break;  // warp-uniform
-    const bool done = (st[i] >> 32) == epoch && W + 32ull * i + lane < A.slice_end;
-    const unsigned nd = __ballot_sync(kFull, !done);
-    const uint32_t lead = nd ? static_cast<uint32_t>(__ffs(nd) - 1) : 32u;
-    const uint32_t cnt = lane < static_cast<int>(lead) ? static_cast<uint32_t>(st[i]) : 0u;
-    unsigned long long v = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned long long y = __shfl_up_sync(kFull, v, o);
-      if (lane >= o) v += y;
-    }
-    if (lane < static_cast<int>(lead)) st_gpu(A.incl + W + 32ull * i + lane, base + v);
-    base += __shfl_sync(kFull, v, 31);
-    j += lead;
-    stop = lead < 32;
-  }
+  const uint64_t j = static_cast<uint64_t>(kPer) * stop + (stop < 32 ? __shfl_sync(kFull, lead, stop) : 0);
   if (j == 0) return W;
+  // exclusive prefix of the lane sums (64-bit: counts are exact past slice_cap)
+  unsigned long long v = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
+  }
+  const unsigned long long end = base + __shfl_sync(kFull, v, 31);
+  unsigned long long run = base + v - sum;
+#pragma unroll
+  for (int i = 0; i < kPer; ++i)
+    if (i < lead) {
+      run += static_cast<uint32_t>(st[i]);
+      st_gpu(A.incl + x0 + i, run);
+    }
   W += j;
   fence_gpu();  // every lane's incl stores before the new watermark
   __syncwarp();
   if (lane == 0) {
-    if (W == A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, base);
+    if (W == A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, end);
     fence_gpu();
     st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrWatermark, W);
   }
@@ -304,6 +316,7 @@ __device__ __forceinline__ void copy_slices(const ScanArgs& A, uint64_t c, int l
 // by running scanning warps, so it cannot deadlock on CTAs that are not
 // resident.
 __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
+  if (A.plan.diag & 256) return;  // diagnostics: no gather warp
   unsigned long long* lock = A.counters + kCtrLock;
   uint64_t claim = ~0ull;
   bool claims_done = false;
