@@ -1,7 +1,7 @@
 // Kernel-family dispatch, the SMAG prepare kernel and launch bookkeeping.
 #include <atomic>
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 
 #include "scan_launch.h"
@@ -40,20 +40,20 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 unsigned long long kernel_launch_count() { return g_launches.load(); }
 
 cudaError_t allow_max_smem(const void* kernel, size_t need) {
+  // The limit only ever grows to what a launch needs (not the device's
+  // opt-in maximum): the driver sizes the shared-memory carveout, hence what
+  // is left for L1, from it.
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, size_t> set;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
-  if (done.count({kernel, dev})) return cudaSuccess;
-  int optin = 0;
-  e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  size_t& cur = set[{kernel, dev}];
+  if (cur >= need) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(need));
   if (e != cudaSuccess) return e;
-  if (need > static_cast<size_t>(optin)) return cudaErrorInvalidValue;
-  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-  if (e != cudaSuccess) return e;
-  done.insert({kernel, dev});
+  cur = need;
   return cudaSuccess;
 }
 

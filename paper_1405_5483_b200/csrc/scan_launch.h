@@ -120,8 +120,8 @@ cudaError_t launch_staged_exact(const ScanArgs& a, cudaStream_t stream, int grid
 cudaError_t launch_staged_hashed(const ScanArgs& a, cudaStream_t stream, int grid);
 cudaError_t launch_staged_codes(const ScanArgs& a, cudaStream_t stream, int grid);
 void count_launch();
-// Raises a kernel's dynamic shared-memory limit to the device's opt-in
-// maximum, once per (kernel, device); thread-safe.
+// Raises a kernel's dynamic shared-memory limit to `need` on the current
+// device when it is lower (per (kernel, device); thread-safe).
 cudaError_t allow_max_smem(const void* kernel, size_t need);
 
 }  // namespace magb
