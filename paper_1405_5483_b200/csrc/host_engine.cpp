@@ -64,9 +64,9 @@ struct Workspace {
   unsigned long long* ctrl = nullptr;
   uint32_t parity = 0;
   bool dirty = false;
-  uint32_t epoch = 0;                  // tag of the last search in slice_state
-  uint64_t* slice_state = nullptr;     // per slice: epoch << 32 | count
-  uint64_t* incl = nullptr;            // per slice: inclusive prefix of counts
+  uint32_t* slice_count = nullptr;     // per slice: match count
+  uint64_t* group_word = nullptr;      // per 32-slice group: slices done << 40 | count (zero between searches)
+  uint64_t* group_incl = nullptr;      // per group: inclusive prefix of counts
   size_t slices_cap = 0;
   uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
   uint64_t* out = nullptr;             // sorted matches (same capacity)
@@ -85,8 +85,9 @@ struct Workspace {
   ~Workspace() {
     cudaSetDevice(device);
     if (ctrl) cudaFree(ctrl);
-    if (slice_state) cudaFree(slice_state);
-    if (incl) cudaFree(incl);
+    if (slice_count) cudaFree(slice_count);
+    if (group_word) cudaFree(group_word);
+    if (group_incl) cudaFree(group_incl);
     if (staging) cudaFree(staging);
     if (out) cudaFree(out);
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -237,7 +238,7 @@ constexpr size_t kCounters = 8;
 constexpr size_t kCtrlWords = kCtrWords;
 
 struct SearchGeometry {
-  uint64_t samples, slice_samples, tail_samples, big_slices, num_slices, slice_cap;
+  uint64_t samples, slice_samples, num_slices, slice_cap;
   uint32_t bps;  // text bytes per sample
 };
 
@@ -267,19 +268,7 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
   g.samples = filter_reads(P, n);
   g.bps = static_cast<uint32_t>(bytes_per_sample(P));
   g.slice_samples = slice_samples_for(e, g.samples);
-  // The last wave of the grid runs tail slices 8x finer (about one big slice
-  // per scanning warp), so the warps run out of work together.
-  const uint64_t unit = step_unit(P);
-  g.tail_samples = std::min<uint64_t>(g.slice_samples,
-                                      std::max<uint64_t>(unit, (g.slice_samples / 8 + unit - 1) / unit * unit));
-  uint64_t tail = std::min<uint64_t>(g.samples / 2, static_cast<uint64_t>(e->sm_count) * P.nwarps * g.slice_samples);
-#ifdef MAG_B200_DIAGNOSTICS
-  if (const char* d = std::getenv("MAG_B200_DIAG"))
-    if (std::atoi(d) & 1024) tail = 0;  // profiling: uniform slices
-#endif
-  g.big_slices = g.samples > tail ? (g.samples - tail) / g.slice_samples : 0;
-  const uint64_t rest = g.samples - g.big_slices * g.slice_samples;
-  g.num_slices = g.big_slices + (rest + g.tail_samples - 1) / g.tail_samples;
+  g.num_slices = (g.samples + g.slice_samples - 1) / g.slice_samples;
   if (cap_override) {
     g.slice_cap = cap_override;
   } else {
@@ -302,8 +291,6 @@ ScanArgs geometry_args(const SearchGeometry& g) {
   ScanArgs a{};
   a.samples = g.samples;
   a.slice_samples = g.slice_samples;
-  a.big_slices = g.big_slices;
-  a.tail_samples = g.tail_samples;
   a.num_slices = g.num_slices;
   return a;
 }
@@ -333,21 +320,24 @@ mag_status ensure_ws(Workspace* w, const SearchGeometry& g, cudaStream_t st) {
     MAG_CUDA(cudaMalloc(&w->ctrl, 2 * kCtrlWords * sizeof(unsigned long long)));
     w->dirty = true;
   }
-  if (w->dirty) {  // new, or a search failed half-way: both halves from zero
+  if (w->dirty) {  // new, or a search failed half-way: control words and group words from zero
     MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long), st));
+    if (w->group_word) MAG_CUDA(cudaMemsetAsync(w->group_word, 0, w->slices_cap / kGroup * sizeof(uint64_t), st));
     w->parity = 0;
     w->dirty = false;
   }
   if (w->slices_cap < std::max<uint64_t>(1, g.num_slices)) {
-    if (w->slice_state) MAG_CUDA(cudaFree(w->slice_state));
-    if (w->incl) MAG_CUDA(cudaFree(w->incl));
-    w->slice_state = w->incl = nullptr;
+    if (w->slice_count) MAG_CUDA(cudaFree(w->slice_count));
+    if (w->group_word) MAG_CUDA(cudaFree(w->group_word));
+    if (w->group_incl) MAG_CUDA(cudaFree(w->group_incl));
+    w->slice_count = nullptr;
+    w->group_word = w->group_incl = nullptr;
     w->slices_cap = 0;
-    const size_t cap = std::max<uint64_t>(1, g.num_slices);
-    MAG_CUDA(cudaMalloc(&w->slice_state, cap * sizeof(uint64_t)));
-    MAG_CUDA(cudaMalloc(&w->incl, cap * sizeof(uint64_t)));
-    // epoch 0 is never a search's tag: fresh states read "not published"
-    MAG_CUDA(cudaMemsetAsync(w->slice_state, 0, cap * sizeof(uint64_t), st));
+    const size_t cap = (std::max<uint64_t>(1, g.num_slices) + kGroup - 1) / kGroup * kGroup;
+    MAG_CUDA(cudaMalloc(&w->slice_count, cap * sizeof(uint32_t)));
+    MAG_CUDA(cudaMalloc(&w->group_word, cap / kGroup * sizeof(uint64_t)));
+    MAG_CUDA(cudaMalloc(&w->group_incl, cap / kGroup * sizeof(uint64_t)));
+    MAG_CUDA(cudaMemsetAsync(w->group_word, 0, cap / kGroup * sizeof(uint64_t), st));
     w->slices_cap = cap;
   }
   const size_t cap = std::max<size_t>(1, g.num_slices * g.slice_cap);
@@ -383,7 +373,6 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   w->num_slices = g.num_slices;
   w->slice_cap = g.slice_cap;
   w->slice_samples = g.slice_samples;
-  if (++w->epoch == 0) w->epoch = 1;
   unsigned long long* counters = w->ctrl + w->parity * kCtrlWords;
   unsigned long long* next_ctrl = w->ctrl + (w->parity ^ 1u) * kCtrlWords;
   ScanArgs a = geometry_args(g);
@@ -415,9 +404,9 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   a.nwarps = P.nwarps;
   a.staging = w->staging;
   a.slice_cap = static_cast<uint32_t>(std::min<uint64_t>(g.slice_cap, 0xfffffff0u));
-  a.epoch = w->epoch;
-  a.slice_state = w->slice_state;
-  a.incl = w->incl;
+  a.slice_count = w->slice_count;
+  a.group_word = w->group_word;
+  a.group_incl = w->group_incl;
   a.out = w->out;
   a.out_cap = w->out_cap;
   a.counters = counters;
@@ -907,7 +896,9 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
       }
       MAG_CUDA(cudaEventRecord(w->chunk_ev[ci], w->copy_stream));
       // slices whose bytes (plus the pattern reach) have fully arrived
-      const uint64_t ready = copied == len ? slices : (copied > reach ? slices_ending_by(sg, copied - reach) : 0);
+      // (launches end on gather-group boundaries: a group never spans two)
+      const uint64_t ready =
+          copied == len ? slices : (copied > reach ? slices_ending_by(sg, copied - reach) / kGroup * kGroup : 0);
       ranges.push_back(SliceRange{slices_done, ready, w->chunk_ev[ci]});
       slices_done = std::max(slices_done, ready);
       ++ci;

@@ -191,23 +191,25 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
 }
 
 // ------------------------------------------------------------ ordered gather
-// Slice end (whole warp): the slice's staged matches become visible before
-// its state says "done with `count` matches".
-// The largest slice count (staging overflow check, learned density) is a
-// fire-and-forget reduction.
+// Slice end (whole warp): the slice's staged matches and its count become
+// visible before its group word says "one more slice done".  The largest
+// slice count (staging overflow check, learned density) is a fire-and-forget
+// reduction.
 __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
   if (A.plan.diag & 512) return;  // diagnostics: no publication (no gather)
-  fence_gpu();  // every lane's staged matches before the state
+  if (lane == 0) A.slice_count[slice] = count;
+  fence_gpu();  // every lane's staged matches (and the count) before the group word
   __syncwarp();
   if (lane == 0) {
-    st_gpu(A.slice_state + slice, (static_cast<uint64_t>(A.epoch) << 32) | count);
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.group_word + slice / kGroup), (1ull << 40) | count);
     if (count) atomicMax(A.counters + kCtrMax, static_cast<unsigned long long>(count));
   }
   __syncwarp();
 }
 
-// A warp leaves the kernel: its candidate count joins the counters; the last warp of the final launch publishes them to the host and
-// clears the next search's control words.
+// A warp leaves the kernel: its candidate count joins the counters; the
+// last warp of the final launch publishes them to the host and clears the
+// next search's control words.
 __device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long cands, int lane) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) cands += __shfl_xor_sync(kFull, cands, o);
@@ -230,30 +232,29 @@ __device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long 
 }
 
 // Watermark advance (one gather warp at a time, under the advance lock):
-// lane l takes the 32 slices W + 32 l ... W + 32 l + 31, so the published
-// run right above W (up to 1024 slices) is found and prefix-summed with
-// per-lane serial sums and one warp scan; the inclusive prefix counts go to
-// incl[] and the new watermark is stored after them.  About two round trips
-// per advance: far more than the ~250 slices per microsecond the scanning
-// warps publish.  Returns the new W.
-__device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_t W, int lane) {
+// lane l takes the 32 groups W + 32 l ... W + 32 l + 31, so the run of
+// complete groups right above W (up to 1024 groups = 32768 slices) is found
+// and prefix-summed with per-lane serial sums and one warp scan; the
+// inclusive prefix counts go to group_incl[] and the new watermark is stored
+// after them.  Returns the new W (groups).
+__device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_t W, uint64_t gend, int lane) {
   constexpr int kPer = 32;
-  const uint32_t epoch = A.epoch;
-  const uint64_t x0 = W + static_cast<uint64_t>(kPer) * lane;
-  uint64_t st[kPer];
+  const uint64_t g0 = W + static_cast<uint64_t>(kPer) * lane;
+  uint64_t wd[kPer];
 #pragma unroll
-  for (int i = 0; i < kPer; ++i) st[i] = x0 + i < A.slice_end ? ld_gpu(A.slice_state + x0 + i) : 0ull;
-  const unsigned long long base = W == 0 ? 0ull : ld_gpu(A.incl + W - 1);
-  // this lane's leading published slices and their count sum
+  for (int i = 0; i < kPer; ++i) wd[i] = g0 + i < gend ? ld_gpu(A.group_word + g0 + i) : 0ull;
+  const unsigned long long base = W == 0 ? 0ull : ld_gpu(A.group_incl + W - 1);
   int lead = kPer;
-  uint32_t sum = 0;
 #pragma unroll
-  for (int i = kPer - 1; i >= 0; --i)
-    if (static_cast<uint32_t>(st[i] >> 32) != epoch || x0 + i >= A.slice_end) lead = i;
+  for (int i = kPer - 1; i >= 0; --i) {
+    const uint64_t g = g0 + i;
+    const uint64_t want = g < gend ? min(static_cast<uint64_t>(kGroup), A.num_slices - g * kGroup) : ~0ull;
+    if ((wd[i] >> 40) != want) lead = i;
+  }
+  unsigned long long sum = 0;
 #pragma unroll
   for (int i = 0; i < kPer; ++i)
-    if (i < lead) sum += static_cast<uint32_t>(st[i]);
-  // the run ends in the first lane that is not fully published
+    if (i < lead) sum += wd[i] & ((1ull << 40) - 1);
   const unsigned partial = __ballot_sync(kFull, lead < kPer);
   const int stop = partial ? __ffs(partial) - 1 : 32;
   if (lane > stop) {
@@ -262,7 +263,6 @@ __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_
   }
   const uint64_t j = static_cast<uint64_t>(kPer) * stop + (stop < 32 ? __shfl_sync(kFull, lead, stop) : 0);
   if (j == 0) return W;
-  // exclusive prefix of the lane sums (64-bit: counts are exact past slice_cap)
   unsigned long long v = sum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -274,14 +274,14 @@ __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_
 #pragma unroll
   for (int i = 0; i < kPer; ++i)
     if (i < lead) {
-      run += static_cast<uint32_t>(st[i]);
-      st_gpu(A.incl + x0 + i, run);
+      run += wd[i] & ((1ull << 40) - 1);
+      st_gpu(A.group_incl + g0 + i, run);
     }
   W += j;
-  fence_gpu();  // every lane's incl stores before the new watermark
+  fence_gpu();  // every lane's prefix stores before the new watermark
   __syncwarp();
   if (lane == 0) {
-    if (W == A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, end);
+    if (W * kGroup >= A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, end);
     fence_gpu();
     st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrWatermark, W);
   }
@@ -289,44 +289,52 @@ __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_
   return W;
 }
 
-// Copy slices [c, c + 32) (all below the watermark) to their final place.
-__device__ __forceinline__ void copy_slices(const ScanArgs& A, uint64_t c, int lane) {
-  const uint64_t x = c + lane;
-  uint32_t cnt = 0;
-  unsigned long long end = 0;
-  if (x < A.slice_end) {
-    cnt = static_cast<uint32_t>(ld_gpu(A.slice_state + x));
-    end = ld_gpu(A.incl + x);
+// Place group c (below the watermark): its slices' offsets are the group's
+// exclusive prefix plus a warp scan of their counts; copy their staged
+// matches; clear the group word for the next search.
+__device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int lane) {
+  const uint64_t x = c * kGroup + lane;
+  const uint32_t cnt = x < A.num_slices ? __ldcg(A.slice_count + x) : 0u;
+  unsigned long long v = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(kFull, v, o);
+    if (lane >= o) v += y;
   }
+  const unsigned long long base = c == 0 ? 0ull : ld_gpu(A.group_incl + c - 1);
+  const unsigned long long mine = base + v - cnt;
   for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
     const int s = __ffs(m) - 1;
     const uint32_t n = __shfl_sync(kFull, cnt, s);
-    const unsigned long long dst = __shfl_sync(kFull, end, s) - n;
+    const unsigned long long dst = __shfl_sync(kFull, mine, s);
     const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
-    const uint64_t* src = A.staging + (c + s) * A.slice_cap;
+    const uint64_t* src = A.staging + (c * kGroup + s) * A.slice_cap;
     for (uint32_t i = lane; i < cc; i += 32)
       if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
   }
+  if (lane == 0) st_gpu(A.group_word + c, 0ull);
 }
 
-// The gather warp of every CTA.  Two jobs: advancing the watermark (any
-// gather warp that takes the advance lock), and copying: each gather warp
-// claims 32 slices at a time (a cursor per launch) and copies them once the
-// watermark has passed them.  Progress only depends on slices already claimed
-// by running scanning warps, so it cannot deadlock on CTAs that are not
-// resident.
+// The gather warp of every CTA.  Two jobs: advancing the watermark (the
+// warp that takes the advance lock keeps advancing while groups complete),
+// and copying: each gather warp claims one group at a time (a cursor per
+// launch) and places it once the watermark has passed it.  Progress only
+// depends on slices already claimed by running scanning warps, so it cannot
+// deadlock on CTAs that are not resident.
 __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
   if (A.plan.diag & 256) return;  // diagnostics: no gather warp
   unsigned long long* lock = A.counters + kCtrLock;
+  const uint64_t gbeg = A.slice_begin / kGroup;
+  const uint64_t gend = (A.slice_end + kGroup - 1) / kGroup;  // launches end on group boundaries
   uint64_t claim = ~0ull;
   bool claims_done = false;
   uint32_t idle = 0;
   while (true) {
     uint64_t W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
     bool progress = false;
-    // the lock is only tried when the slice at the watermark is published
-    bool ready = false;
-    if (lane == 0 && W < A.slice_end) ready = (ld_gpu(A.slice_state + W) >> 32) == A.epoch;
+    bool ready = false;  // the lock is only tried when the group at the watermark is complete
+    if (lane == 0 && W < gend)
+      ready = (ld_gpu(A.group_word + W) >> 40) == min(static_cast<uint64_t>(kGroup), A.num_slices - W * kGroup);
     if (__shfl_sync(kFull, ready, 0)) {
       unsigned long long got = 1;
       if (lane == 0) got = atomicCAS(lock, 0ull, 1ull);
@@ -334,9 +342,12 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
       if (got == 0) {
         fence_gpu();
         W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
-        const uint64_t W2 = advance_watermark(A, W, lane);
-        progress = W2 != W;
-        W = W2;
+        for (int rounds = 0; rounds < 64 && W < gend; ++rounds) {
+          const uint64_t W2 = advance_watermark(A, W, gend, lane);
+          if (W2 == W) break;
+          progress = true;
+          W = W2;
+        }
         if (lane == 0) {
           fence_gpu();
           atomicExch(lock, 0ull);
@@ -345,24 +356,24 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
     }
     if (!claims_done && claim == ~0ull) {
       unsigned long long c = 0;
-      if (lane == 0) c = atomicAdd(A.copy_cursor, 32ull);
-      c = __shfl_sync(kFull, c, 0) + A.slice_begin;
-      if (c >= A.slice_end)
+      if (lane == 0) c = atomicAdd(A.copy_cursor, 1ull);
+      c = __shfl_sync(kFull, c, 0) + gbeg;
+      if (c >= gend)
         claims_done = true;
       else
         claim = c;
     }
-    if (claim != ~0ull && (claim + 32 <= W || W >= A.slice_end)) {
+    if (claim != ~0ull && claim < W) {
       fence_gpu();
-      copy_slices(A, claim, lane);
+      copy_group(A, claim, lane);
       claim = ~0ull;
       progress = true;
     }
-    if (claims_done && claim == ~0ull && W >= A.slice_end) break;
+    if (claims_done && claim == ~0ull && W >= gend) break;
     if (progress) {
       idle = 0;
     } else {
-      __nanosleep(idle < 8 ? 100 : 500);
+      __nanosleep(idle < 8 ? 100 : 400);
       ++idle;
     }
   }

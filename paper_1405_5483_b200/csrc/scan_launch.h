@@ -10,23 +10,23 @@ namespace magb {
 // Everything one scan launch needs.  Device pointers only.
 //
 // Work decomposition: the filter's samples t in [0, samples) are cut into
-// slices — big_slices slices of slice_samples, then tail slices of
-// tail_samples (smaller, so the last wave of the grid ends together).  A
-// slice is owned by one warp (dynamic ticket) and produces the matches of
-// exactly the candidate windows its samples raise, in (offset, pattern)
-// order, into staging + slice * slice_cap.  A slice is streamed through the
-// warp's ring of shared-memory slots in chunks of chunk_samples samples (TMA
-// bulk copies, one mbarrier per slot).
+// slices of slice_samples.  A slice is owned by one warp (dynamic ticket)
+// and produces the matches of exactly the candidate windows its samples
+// raise, in (offset, pattern) order, into staging + slice * slice_cap.  A
+// slice is streamed through the warp's ring of shared-memory slots in chunks
+// of chunk_samples samples (TMA bulk copies, one mbarrier per slot).
 //
-// Ordered gather (no second kernel): at the end of a slice its owner
-// publishes (epoch << 32 | count) in slice_state[slice].  The last warp of
-// every CTA is a gather warp: under a lock, one of them at a time advances
-// the watermark (counters[0]) over published slices, writing their
-// inclusive prefix counts into incl[]; every gather warp claims 32 slices at
-// a time below the watermark and copies their staged matches to
-// out[prefix..].  The last warp to leave the final
-// launch of a search writes the counters to host_ctr (mapped pinned host
-// memory) and zeroes the next search's control words.
+// Ordered gather (no second kernel).  Slices form groups of 32 (kGroup).  At
+// the end of a slice its owner stores the count in slice_count[] and adds
+// (1 << 40 | count) to its group's word.  The last warp of every CTA is a
+// gather warp: under a lock, one of them at a time advances the watermark
+// (counters[kCtrWatermark], in groups) over complete groups, writing their
+// inclusive prefix counts into group_incl[]; every gather warp claims one
+// group at a time below the watermark, places its slices (a warp scan of
+// their counts) and copies their staged matches to out[prefix..].  The last
+// warp to leave the final launch of a search writes the counters to
+// host_ctr (mapped pinned host memory) and zeroes the next search's control
+// words.
 struct ScanArgs {
   ScanPlan plan;
   const uint8_t* text;          // 16-byte aligned
@@ -45,22 +45,20 @@ struct ScanArgs {
   uint32_t vmask;
   uint32_t zero;                // always 0; opaque to the compiler (orders slot reads before TMA refills)
   uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping, n verify-all
-  uint64_t slice_samples;       // big slices: multiple of chunk_samples
-  uint64_t big_slices;          // slices [0, big_slices) are big, the rest tail slices
-  uint64_t tail_samples;        // tail slices: multiple of chunk_samples, <= slice_samples
+  uint64_t slice_samples;       // multiple of chunk_samples
   uint32_t chunk_samples;       // samples per chunk (iterations * advance)
   uint32_t back;                // staged bytes after the last gram (pattern reach)
   uint32_t full_bytes;          // staged bytes of an interior chunk (multiple of 16)
   uint32_t slot_bytes;          // one ring slot (multiple of 16, >= full_bytes + 32)
   uint32_t ring;                // slots per warp
   uint32_t nwarps;              // scanning warps per CTA (the CTA has one more: the gather warp)
-  uint64_t slice_begin, slice_end;  // slices of this launch
+  uint64_t slice_begin, slice_end;  // slices of this launch (whole groups except at the text end)
   uint64_t num_slices;
   uint64_t* staging;            // num_slices * slice_cap packed matches
   uint32_t slice_cap;           // multiple of 16 (slices never share a 128-byte line)
-  uint32_t epoch;               // this search's tag in slice_state
-  uint64_t* slice_state;        // per slice: epoch << 32 | exact match count (even past slice_cap)
-  uint64_t* incl;               // per slice: inclusive prefix of counts (valid below the watermark)
+  uint32_t* slice_count;        // per slice: exact match count (even past slice_cap)
+  uint64_t* group_word;         // per group: completed slices << 40 | match count (zeroed after its copy)
+  uint64_t* group_incl;         // per group: inclusive prefix of counts (valid below the watermark)
   uint64_t* out;                // sorted output
   uint64_t out_cap;
   unsigned long long* counters; // control words (kCtr*)
@@ -75,19 +73,17 @@ struct ScanArgs {
 };
 
 // Slice geometry (host and device).
-MAG_HD uint64_t slice_t0(const ScanArgs& a, uint64_t x) {
-  return x < a.big_slices ? x * a.slice_samples
-                          : a.big_slices * a.slice_samples + (x - a.big_slices) * a.tail_samples;
-}
+constexpr unsigned kGroup = 32;  // slices per gather group
+MAG_HD uint64_t slice_t0(const ScanArgs& a, uint64_t x) { return x * a.slice_samples; }
 MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
-  const uint64_t t = slice_t0(a, x) + (x < a.big_slices ? a.slice_samples : a.tail_samples);
+  const uint64_t t = (x + 1) * a.slice_samples;
   return t < a.samples ? t : a.samples;
 }
 
 // Control words of one search (a half of the workspace's ctrl array).
 // Each group has its own 128-byte line, so the scanning warps' ticket
 // atomics never share a line with the gather warps' polls.
-constexpr unsigned kCtrWatermark = 0;  // gather watermark
+constexpr unsigned kCtrWatermark = 0;  // gather watermark (groups)
 constexpr unsigned kCtrTotal = 1;      // total matches (set when the watermark reaches the end)
 constexpr unsigned kCtrLock = 16;      // watermark-advance lock
 constexpr unsigned kCtrCands = 32;     // filter candidates
