@@ -68,8 +68,12 @@ __device__ __forceinline__ uint64_t ld_gpu(const uint64_t* p) {
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-// Release/acquire fence at GPU scope (lighter than __threadfence's fence.sc).
+// Fences at GPU scope.  An acquire (fence.acq_rel, ld.acquire) invalidates the
+// SM's whole L1 (CCTL.IVALL), which the scanning warps' screen and pattern
+// loads rely on: the scanning warps only ever release (MEMBAR, no IVALL);
+// the gather warps acquire once per lock or copy claim.
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -198,7 +202,7 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
 __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
   if (A.plan.diag & 512) return;  // diagnostics: no publication (no gather)
   if (lane == 0) A.slice_count[slice] = count;
-  fence_gpu();  // every lane's staged matches (and the count) before the group word
+  fence_release();  // every lane's staged matches (and the count) before the group word
   __syncwarp();
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(A.group_word + slice / kGroup), (1ull << 40) | count);
@@ -216,7 +220,7 @@ __device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long 
   unsigned long long old = 0;
   if (lane == 0) {
     if (cands) atomicAdd(A.counters + kCtrCands, cands);
-    fence_gpu();
+    fence_release();
     old = atomicAdd(A.exits, 1ull);
   }
   old = __shfl_sync(kFull, old, 0);
@@ -278,11 +282,11 @@ __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_
       st_gpu(A.group_incl + g0 + i, run);
     }
   W += j;
-  fence_gpu();  // every lane's prefix stores before the new watermark
+  fence_release();  // every lane's prefix stores before the new watermark
   __syncwarp();
   if (lane == 0) {
     if (W * kGroup >= A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, end);
-    fence_gpu();
+    fence_release();
     st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrWatermark, W);
   }
   __syncwarp();
@@ -349,7 +353,7 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
           W = W2;
         }
         if (lane == 0) {
-          fence_gpu();
+          fence_release();
           atomicExch(lock, 0ull);
         }
       }
