@@ -429,7 +429,6 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     ++li;
     const uint64_t ctas = std::max<uint64_t>(1, (end - begin + P.nwarps - 1) / P.nwarps);
     const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
-    a.launch_warps = static_cast<uint32_t>(grid) * (P.nwarps + 1);
     a.final_launch = final_launch ? 1u : 0u;
     MAG_CUDA(timed_launch(a, st, grid));
     return MAG_OK;

@@ -211,29 +211,17 @@ __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice,
   __syncwarp();
 }
 
-// A warp leaves the kernel: its candidate count joins the counters; the
-// last warp of the final launch publishes them to the host and clears the
-// next search's control words.
-__device__ __forceinline__ void warp_exit(const ScanArgs& A, unsigned long long cands, int lane) {
+// A scanning warp leaves the kernel: its candidate count joins the counters.
+__device__ __forceinline__ void scan_exit(const ScanArgs& A, unsigned long long cands, int lane) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) cands += __shfl_xor_sync(kFull, cands, o);
-  unsigned long long old = 0;
-  if (lane == 0) {
-    if (cands) atomicAdd(A.counters + kCtrCands, cands);
-    fence_release();
-    old = atomicAdd(A.exits, 1ull);
-  }
-  old = __shfl_sync(kFull, old, 0);
-  if (old + 1 != A.launch_warps || !A.final_launch) return;
-  fence_gpu();
-  if (lane < 3) {
-    const unsigned src = lane == 0 ? kCtrCands : (lane == 1 ? kCtrTotal : kCtrMax);
-    const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + src);
-    reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[1 + lane] = v;
-  }
-  for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
-  __threadfence_system();
+  if (lane == 0 && cands) atomicAdd(A.counters + kCtrCands, cands);
 }
+
+// Let the search's gather kernel start now (programmatic dependent launch):
+// its one-warp CTAs run beside the scan on the registers a 15-warp CTA
+// leaves free, and place slices while the scan goes on.
+__device__ __forceinline__ void allow_gather() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Watermark advance (one gather warp at a time, under the advance lock):
 // lane l takes the 32 groups W + 32 l ... W + 32 l + 31, so the run of
@@ -319,12 +307,13 @@ __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int la
   if (lane == 0) st_gpu(A.group_word + c, 0ull);
 }
 
-// The gather warp of every CTA.  Two jobs: advancing the watermark (the
-// warp that takes the advance lock keeps advancing while groups complete),
-// and copying: each gather warp claims one group at a time (a cursor per
-// launch) and places it once the watermark has passed it.  Progress only
-// depends on slices already claimed by running scanning warps, so it cannot
-// deadlock on CTAs that are not resident.
+// A gather warp (scan_dispatch.cu mag_gather_kernel: one per CTA, grid
+// beside the scan).  Two jobs: advancing the watermark (the warp that takes
+// the advance lock keeps advancing while groups complete), and copying: each
+// gather warp claims one group at a time (a cursor per launch) and places it
+// once the watermark has passed it.  The scan never waits for the gather, and
+// the gather only waits for slices the scan's running warps have claimed, so
+// nothing can deadlock whether or not the two grids are co-resident.
 __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
   if (A.plan.diag & 256) return;  // diagnostics: no gather warp
   unsigned long long* lock = A.counters + kCtrLock;

@@ -57,14 +57,15 @@ struct DirectScanner {
   uint64_t* bars;     // [DEPTH]
   DirectDesc* desc;   // [DEPTH]
   uint32_t pqn, fill, cands32;
-  uint32_t pbase_lo;  // low 32 bits of the current slice's first sample
   uint32_t cur_slice; // the current slice
   uint64_t* out;
   // a step: 256 16-byte samples (4 KiB) or 256 8-byte samples (2 KiB)
   static constexpr uint32_t kStepBytes = W == 16 ? 4096u : 2048u;
   static constexpr uint32_t kStep = kStepBytes / W;
   static constexpr int kPer = kStep / 32;  // samples per lane per step
-  uint32_t pend_w[kPer], pend_b[kPer], pend_k[kPer], pend_pos;  // screen loads in flight
+  // screen loads in flight: word and key (the key's low 5 bits are its
+  // screen bit within the word: l2_bits >= 16)
+  uint32_t pend_w[kPer], pend_k[kPer], pend_pos;
   // producer cursor (warp-uniform)
   unsigned long long p_t;
   uint32_t p_left;
@@ -74,8 +75,8 @@ struct DirectScanner {
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
-        pbase_lo(0), cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
-    for (int i = 0; i < kPer; ++i) pend_w[i] = pend_b[i] = pend_k[i] = 0;
+        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
+    for (int i = 0; i < kPer; ++i) pend_w[i] = pend_k[i] = 0;
     pend_pos = 0;
   }
 
@@ -97,11 +98,8 @@ struct DirectScanner {
         p_done = true;
         break;
       }
+      // every slice below num_slices holds samples (num_slices = ceil(samples / S))
       const unsigned long long t0 = slice_t0(A, x), t1 = slice_t1(A, x);
-      if (t1 <= t0) {
-        publish_slice(A, x, 0, lane);
-        continue;
-      }
       slice = static_cast<uint32_t>(x);
       p_t = t0;
       p_left = static_cast<uint32_t>(t1 - t0);
@@ -188,8 +186,7 @@ struct DirectScanner {
       // the window key is the sample's gram hash (direct plans: key_gram)
       const uint32_t key = h[i];
       pend_k[i] = key;
-      const uint32_t sb = lb ? screen_bit(key, lb) : 0u;
-      pend_b[i] = sb;  // resolve() shifts in wrap mode: bit sb & 31
+      const uint32_t sb = lb ? screen_bit(key, lb) : 0u;  // resolve() shifts by key: bit sb & 31
       // the screen word is only consumed by resolve() one step later.  W = 16
       // plans (a quarter to most samples hit: cfg2/cfg4) issue it as one
       // predicated load, no branch per sample (cfg2 +5%); W = 8 plans (rare
@@ -212,7 +209,7 @@ struct DirectScanner {
   __device__ __forceinline__ void resolve() {
     uint32_t surv = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) surv |= (__funnelshift_r(pend_w[i], pend_w[i], pend_b[i]) & 1u) << i;
+    for (int i = 0; i < kPer; ++i) surv |= (__funnelshift_r(pend_w[i], pend_w[i], pend_k[i]) & 1u) << i;
     if (__any_sync(kFull, surv != 0)) {
 #pragma unroll
       for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 32u * W * i);
@@ -228,7 +225,6 @@ struct DirectScanner {
     if ((d.lim_flags >> 16) & 1u) {
       fill = 0;
       pqn = 0;
-      pbase_lo = d.t_lo;
       cur_slice = d.slice;
       out = A.staging + static_cast<size_t>(d.slice) * A.slice_cap;
     } else {
@@ -238,7 +234,8 @@ struct DirectScanner {
 
   __device__ __forceinline__ void process(const DirectDesc& d, const uint32_t (&h)[kPer]) {
     const uint32_t lim = d.lim_flags & 0xffffu, flags = d.lim_flags >> 16;
-    pend_pos = W * (d.t_lo - pbase_lo) + W * lane;  // slices < 2^32 samples
+    // sample offset within the slice (slices < 2^32 samples; low words suffice)
+    pend_pos = W * (d.t_lo - static_cast<uint32_t>(slice_t0(A, cur_slice))) + W * lane;
     filter(h, lim);
     if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
     if (flags & 2u) {
@@ -291,17 +288,18 @@ struct DirectScanner {
       process(d, h);
       j = j + 1 == DEPTH ? 0 : j + 1;
     }
-    warp_exit(A, cands32, lane);
+    scan_exit(A, cands32, lane);
   }
 };
 
-// NT: launch bound (scanning warps + the gather warp).
+// NT: launch bound (15 warps are launched: the 16th warp's registers host
+// the search's gather kernel).
 template <int H, int DEPTH, int NT, int W>
 __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
   const size_t tbytes = align16(A.plan.table_bytes);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nw = static_cast<int>(A.nwarps);  // scanning warps; warp nw gathers
+  const int nw = static_cast<int>(A.nwarps);
   uint8_t* p = smem + tbytes;
   uint2* pq = reinterpret_cast<uint2*>(p) + static_cast<size_t>(warp) * kDirectProbeCap;
   p += align16(size_t(nw) * kDirectProbeCap * 8);
@@ -310,44 +308,39 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
   DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
   p += size_t(nw) * DEPTH * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
-  const bool scanning = warp < nw;
-  if (scanning && lane == 0) {
+  allow_gather();
+  if (lane == 0) {
     for (int j = 0; j < DEPTH; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
   DirectScanner<H, DEPTH, W> ds(A, smem, pq, slots, bars, desc, lane);
-  if (scanning) ds.start();
+  ds.start();
   {
     const uint4* src = static_cast<const uint4*>(A.table);
     uint4* dst = reinterpret_cast<uint4*>(smem);
     for (size_t i = threadIdx.x; i < tbytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
     __syncthreads();
   }
-  if (scanning) {
-    ds.run();
-  } else {
-    gather_warp_run(A, lane);
-    warp_exit(A, 0, lane);
-  }
+  ds.run();
 }
 
 template <int H, int DEPTH, int NT, int W>
 cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  if ((a.nwarps + 1) * 32 > NT) return cudaErrorInvalidConfiguration;
+  if (a.nwarps * 32 > NT) return cudaErrorInvalidConfiguration;
   auto k = mag_direct_kernel<H, DEPTH, NT, W>;
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   (void)cudaGetLastError();
-  k<<<grid, (a.nwarps + 1) * 32, smem, stream>>>(a);
+  k<<<grid, a.nwarps * 32, smem, stream>>>(a);
   count_launch();
   return cudaGetLastError();
 }
 
 template <int H>
 cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  // 16 warps per CTA (15 scanning + the gather warp): a 17th warp would cut
-  // every warp to 96 registers (5 warps on one SM sub-partition)
+  // 15 warps per CTA: the gather kernel's one-warp CTAs take the 16th
+  // warp's registers (a 17th warp would cut every warp to 96 registers)
   if (a.plan.q == 8) {  // 8-byte samples (m >= 15)
     if constexpr (H <= 4) return launch_direct_hd<H, kDirectDepth, 512, 8>(a, stream, grid, smem);
     return cudaErrorInvalidValue;

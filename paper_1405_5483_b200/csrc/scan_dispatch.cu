@@ -4,12 +4,38 @@
 #include <map>
 #include <utility>
 
-#include "scan_launch.h"
+#include "kern_common.cuh"
 
 namespace magb {
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};
+
+// The search's gather grid: one warp per CTA, launched as a programmatic
+// dependent of the scan so it runs beside it (kern_common.cuh
+// gather_warp_run).  The last gather warp of the final launch waits for the
+// scan grid to complete (its candidate counts), then publishes the counters
+// to the mapped host words and clears the next search's control words.
+__global__ void __launch_bounds__(32, 16) mag_gather_kernel(const __grid_constant__ ScanArgs A) {
+  const int lane = threadIdx.x & 31;
+  gather_warp_run(A, lane);
+  unsigned long long old = 0;
+  if (lane == 0) {
+    fence_release();
+    old = atomicAdd(A.exits, 1ull);
+  }
+  old = __shfl_sync(kFull, old, 0);
+  if (old + 1 != gridDim.x || !A.final_launch) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  fence_gpu();
+  if (lane < 3) {
+    const unsigned src = lane == 0 ? kCtrCands : (lane == 1 ? kCtrTotal : kCtrMax);
+    const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + src);
+    reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[1 + lane] = v;
+  }
+  for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
+  __threadfence_system();
+}
 
 // SMAG prepare (encode_text qgram.cpp:29-37) on the device.
 __global__ void mag_encode_kernel(const ScanPlan P, const uint8_t* __restrict__ text, uint64_t nq,
@@ -57,12 +83,33 @@ cudaError_t allow_max_smem(const void* kernel, size_t need) {
   return cudaSuccess;
 }
 
-cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
+namespace {
+cudaError_t launch_scan_only(const ScanArgs& a, cudaStream_t stream, int grid) {
   if (a.plan.direct) return launch_direct(a, stream, grid);
   if (a.plan.roll) return launch_roll(a, stream, grid);
   if (a.plan.smag) return launch_staged_codes(a, stream, grid);
   if (a.plan.gram_mode == kGramHashed) return launch_staged_hashed(a, stream, grid);
   return launch_staged_exact(a, stream, grid);
+}
+}  // namespace
+
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
+  cudaError_t e = launch_scan_only(a, stream, grid);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, mag_gather_kernel, a);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n, const uint8_t* map,

@@ -16,15 +16,17 @@ namespace magb {
 // slice is streamed through the warp's ring of shared-memory slots in chunks
 // of chunk_samples samples (TMA bulk copies, one mbarrier per slot).
 //
-// Ordered gather (no second kernel).  Slices form groups of 32 (kGroup).  At
-// the end of a slice its owner stores the count in slice_count[] and adds
-// (1 << 40 | count) to its group's word.  The last warp of every CTA is a
-// gather warp: under a lock, one of them at a time advances the watermark
+// Ordered gather (concurrent, no second pass).  Slices form groups of 32
+// (kGroup).  At the end of a slice its owner stores the count in
+// slice_count[] and adds (1 << 40 | count) to its group's word.  A gather
+// grid of one-warp CTAs runs beside the scan (programmatic dependent launch
+// into the registers a 15-warp scan CTA leaves free): under a lock, one
+// gather warp at a time advances the watermark
 // (counters[kCtrWatermark], in groups) over complete groups, writing their
 // inclusive prefix counts into group_incl[]; every gather warp claims one
 // group at a time below the watermark, places its slices (a warp scan of
 // their counts) and copies their staged matches to out[prefix..].  The last
-// warp to leave the final launch of a search writes the counters to
+// gather warp of the final launch of a search writes the counters to
 // host_ctr (mapped pinned host memory) and zeroes the next search's control
 // words.
 struct ScanArgs {
@@ -51,7 +53,7 @@ struct ScanArgs {
   uint32_t full_bytes;          // staged bytes of an interior chunk (multiple of 16)
   uint32_t slot_bytes;          // one ring slot (multiple of 16, >= full_bytes + 32)
   uint32_t ring;                // slots per warp
-  uint32_t nwarps;              // scanning warps per CTA (the CTA has one more: the gather warp)
+  uint32_t nwarps;              // warps per scan CTA (the gather grid: one warp per CTA)
   uint64_t slice_begin, slice_end;  // slices of this launch (whole groups except at the text end)
   uint64_t num_slices;
   uint64_t* staging;            // num_slices * slice_cap packed matches
@@ -65,7 +67,6 @@ struct ScanArgs {
   unsigned long long* ticket;   // slice ticket of this launch (zeroed)
   unsigned long long* exits;    // warps of this launch that have left (zeroed)
   unsigned long long* copy_cursor;  // gather warps' copy claims of this launch (zeroed)
-  uint32_t launch_warps;        // warps of this launch (grid * (nwarps + 1))
   uint32_t final_launch;        // 1: the search's last launch publishes the counters
   unsigned long long* host_ctr; // mapped pinned host words: [1] candidates [2] matches [3] max slice count
   unsigned long long* reset;    // zeroed by the final launch's last warp (next search's control words)
@@ -98,8 +99,9 @@ struct LaunchShape {
   unsigned threads;
 };
 
-// Enqueues the fused filter + verify + ordered-gather kernel (persistent,
-// `grid` CTAs).
+// Enqueues the fused filter + verify kernel (persistent, `grid` CTAs) and
+// beside it, as its programmatic dependent, the gather grid (`grid` one-warp
+// CTAs) that places the slices' matches in order.
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid);
 
 // SMAG prepare: codes[u] = mask index of gram u, for u < n/q.

@@ -380,15 +380,16 @@ struct RollScanner {
       produce(j);  // the slot is free again
       j = j + 1 == kRollDepth ? 0 : j + 1;
     }
-    warp_exit(A, cands32, lane);
+    scan_exit(A, cands32, lane);
   }
 };
 
-// 15 scanning warps + the gather warp (16 warps: 128 registers each)
+// launch bound: 15 warps are launched (the gather kernel takes the 16th's registers)
 constexpr int kRollThreads = 16 * 32;
 
 template <int Q, int H>
 __global__ void __launch_bounds__(kRollThreads, 1) mag_roll_kernel(const __grid_constant__ ScanArgs A) {
+  allow_gather();
   extern __shared__ __align__(128) uint8_t smem[];
   const size_t tbytes = align16(A.plan.table_bytes);
   {
@@ -407,11 +408,6 @@ __global__ void __launch_bounds__(kRollThreads, 1) mag_roll_kernel(const __grid_
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * kRollDepth;
   p += static_cast<size_t>(nw) * kRollDepth * 8;
   uint16_t* list = reinterpret_cast<uint16_t*>(p) + static_cast<size_t>(warp) * kRollList;
-  if (warp == nw) {  // the CTA's gather warp
-    gather_warp_run(A, threadIdx.x & 31);
-    warp_exit(A, 0, threadIdx.x & 31);
-    return;
-  }
   if ((threadIdx.x & 31) == 0) {
     for (int j = 0; j < kRollDepth; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -423,11 +419,11 @@ __global__ void __launch_bounds__(kRollThreads, 1) mag_roll_kernel(const __grid_
 
 template <int Q, int H>
 cudaError_t launch_roll_qh(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  if ((a.nwarps + 1) * 32 > kRollThreads) return cudaErrorInvalidConfiguration;
+  if (a.nwarps * 32 > kRollThreads) return cudaErrorInvalidConfiguration;
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(mag_roll_kernel<Q, H>), smem);
   if (e != cudaSuccess) return e;
   (void)cudaGetLastError();
-  mag_roll_kernel<Q, H><<<grid, (a.nwarps + 1) * 32, smem, stream>>>(a);
+  mag_roll_kernel<Q, H><<<grid, a.nwarps * 32, smem, stream>>>(a);
   count_launch();
   return cudaGetLastError();
 }

@@ -813,12 +813,13 @@ struct Scanner {
       ++cons;
       issue();
     }
-    warp_exit(A, cands + cands32, lane);
+    scan_exit(A, cands + cands32, lane);
   }
 };
 
 template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK, bool A4>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
+  allow_gather();
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
   Smem S;
@@ -850,13 +851,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __gri
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == static_cast<int>(A.nwarps)) {  // the CTA's gather warp
-    gather_warp_run(A, lane);
-    warp_exit(A, 0, lane);
-    return;
-  }
-  Scanner<GM, E, TSMEM, QW, CMP, CK, A4> sc(A, S, lane, warp);
+  Scanner<GM, E, TSMEM, QW, CMP, CK, A4> sc(A, S, threadIdx.x & 31, threadIdx.x >> 5);
   sc.run();
 }
 template <int GM, typename E, bool TSMEM, int QW, int CMP = 0, int CK = 0, bool A4 = false>
@@ -865,7 +860,7 @@ cudaError_t launch_t(const ScanArgs& a, cudaStream_t st, int grid, size_t smem) 
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   (void)cudaGetLastError();  // a stale error of another runtime user (e.g. torch) is not ours
-  k<<<grid, (a.nwarps + 1) * 32, smem, st>>>(a);
+  k<<<grid, a.nwarps * 32, smem, st>>>(a);
   count_launch();
   return cudaGetLastError();
 }
