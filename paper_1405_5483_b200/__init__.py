@@ -21,9 +21,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmag_b200.so")
 # Profiling only (tools/): MAG_B200_PROFILE_LIB=diag loads the in-tree
-# diagnostics build (`make diag`), whose searches honour MAG_B200_DIAG.
-if os.environ.get("MAG_B200_PROFILE_LIB") == "diag":
-    LIB_PATH = os.path.join(_HERE, "libmag_b200_diag.so")
+# diagnostics build (`make diag`), whose searches honour MAG_B200_DIAG;
+# MAG_B200_PROFILE_LIB=<name> loads libmag_b200_<name>.so (A/B builds).
+if os.environ.get("MAG_B200_PROFILE_LIB"):
+    LIB_PATH = os.path.join(_HERE, f"libmag_b200_{os.environ['MAG_B200_PROFILE_LIB']}.so")
 
 # mag_status (mag.h:26-36)
 MAG_OK = 0

@@ -82,7 +82,7 @@ __device__ __forceinline__ void st_gpu(uint64_t* p, uint64_t v) {
 // 16 pattern bytes at a time against two aligned 16-byte text loads
 // (independent, one round trip per piece) realigned with funnel shifts.
 __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, uint32_t b) { return __funnelshift_r(lo, hi, b); }
-__device__ __noinline__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len) {
+__device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len) {
   const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
   if (a + len + 32 > A.n) {  // near the end of the text: bytewise (no over-read)
     const uint8_t* t = A.text + a;
