@@ -196,13 +196,18 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
 
 // ------------------------------------------------------------ ordered gather
 // Slice end (whole warp): the slice's staged matches and its count become
-// visible before its group word says "one more slice done".  The largest
+// visible before its group word says "one more slice done".  slice_count is
+// zero between searches (the copier clears it), so an empty slice stores
+// nothing and needs no fence (a fence waits ~1 us for the store
+// acknowledgements; most slices of a sparse search are empty).  The largest
 // slice count (staging overflow check, learned density) is a fire-and-forget
 // reduction.
 __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
   if (A.plan.diag & 512) return;  // diagnostics: no publication (no gather)
-  if (lane == 0) A.slice_count[slice] = count;
-  fence_release();  // every lane's staged matches (and the count) before the group word
+  if (count) {
+    if (lane == 0) A.slice_count[slice] = count;
+    fence_release();  // every lane's staged matches (and the count) before the group word
+  }
   __syncwarp();
   if (lane == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(A.group_word + slice / kGroup), (1ull << 40) | count);
@@ -304,6 +309,8 @@ __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int la
     for (uint32_t i = lane; i < cc; i += 32)
       if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
   }
+  // zero between searches: the group word and the nonzero slice counts
+  if (cnt) A.slice_count[x] = 0;
   if (lane == 0) st_gpu(A.group_word + c, 0ull);
 }
 
@@ -320,31 +327,48 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
   const uint64_t gbeg = A.slice_begin / kGroup;
   const uint64_t gend = (A.slice_end + kGroup - 1) / kGroup;  // launches end on group boundaries
   uint64_t claim = ~0ull;
-  bool claims_done = false;
+  bool claims_done = false, advancer = false;
   uint32_t idle = 0;
   while (true) {
     uint64_t W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
     bool progress = false;
     bool ready = false;  // the lock is only tried when the group at the watermark is complete
-    if (lane == 0 && W < gend)
+    if (lane == 0 && !advancer && W < gend)
       ready = (ld_gpu(A.group_word + W) >> 40) == min(static_cast<uint64_t>(kGroup), A.num_slices - W * kGroup);
-    if (__shfl_sync(kFull, ready, 0)) {
+    if (!advancer && __shfl_sync(kFull, ready, 0)) {
       unsigned long long got = 1;
       if (lane == 0) got = atomicCAS(lock, 0ull, 1ull);
       got = __shfl_sync(kFull, got, 0);
       if (got == 0) {
+        // this warp is the advancer until the launch's last group: it polls
+        // the group words itself (one warp spinning on one SM), so the
+        // watermark follows the scan by about one poll
         fence_gpu();
         W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
-        for (int rounds = 0; rounds < 64 && W < gend; ++rounds) {
+        uint32_t spins = 0;
+        while (W < gend) {
           const uint64_t W2 = advance_watermark(A, W, gend, lane);
-          if (W2 == W) break;
-          progress = true;
-          W = W2;
+          if (W2 == W) {
+            __nanosleep(spins < 16 ? 64 : 256);
+            ++spins;
+          } else {
+            spins = 0;
+            progress = true;
+            W = W2;
+            // place a claimed group as soon as the watermark passes it
+            if (claim != ~0ull && claim < W) {
+              fence_gpu();
+              copy_group(A, claim, lane);
+              claim = ~0ull;
+            }
+          }
         }
-        if (lane == 0) {
+        if (lane == 0) {  // the next launch of the search needs the lock
           fence_release();
           atomicExch(lock, 0ull);
         }
+      } else {
+        advancer = true;  // someone else holds the advance for this launch
       }
     }
     if (!claims_done && claim == ~0ull) {
