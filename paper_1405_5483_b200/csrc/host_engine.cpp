@@ -323,6 +323,7 @@ mag_status ensure_ws(Workspace* w, const SearchGeometry& g, cudaStream_t st) {
   if (w->dirty) {  // new, or a search failed half-way: control words and group words from zero
     MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long), st));
     if (w->group_word) MAG_CUDA(cudaMemsetAsync(w->group_word, 0, w->slices_cap / kGroup * sizeof(uint64_t), st));
+    if (w->slice_count) MAG_CUDA(cudaMemsetAsync(w->slice_count, 0, w->slices_cap * sizeof(uint32_t), st));
     w->parity = 0;
     w->dirty = false;
   }
@@ -338,6 +339,7 @@ mag_status ensure_ws(Workspace* w, const SearchGeometry& g, cudaStream_t st) {
     MAG_CUDA(cudaMalloc(&w->group_word, cap / kGroup * sizeof(uint64_t)));
     MAG_CUDA(cudaMalloc(&w->group_incl, cap / kGroup * sizeof(uint64_t)));
     MAG_CUDA(cudaMemsetAsync(w->group_word, 0, cap / kGroup * sizeof(uint64_t), st));
+    MAG_CUDA(cudaMemsetAsync(w->slice_count, 0, cap * sizeof(uint32_t), st));
     w->slices_cap = cap;
   }
   const size_t cap = std::max<size_t>(1, g.num_slices * g.slice_cap);
@@ -484,6 +486,11 @@ mag_status materialize(mag_matches* m) {
     MAG_CUDA(cudaMemcpy(m->keys.data(), w->out, total * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   m->metrics.filter_reads = filter_reads(e->plan, m->n);
   m->metrics.candidates = e->plan.sp.verify_all ? analytic_candidates(e->plan, m->n) : hc[1];
+#ifdef MAG_B200_DIAGNOSTICS
+  if (std::getenv("MAG_B200_TIMELINE"))
+    std::fprintf(stderr, "timeline_ns last_scan_end=%llu watermark_end=%llu last_gather=%llu counters_out=%llu\n",
+                 hc[4], hc[5], hc[6], hc[7]);
+#endif
   m->pending = false;
   release(e, std::move(m->ws));
   return MAG_OK;

@@ -216,17 +216,37 @@ __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice,
   __syncwarp();
 }
 
+// Diagnostics builds (MAG_B200_DIAG bit 2048): a timeline of the search in
+// spare control words, ns since the first scan CTA started (the host prints
+// it): [kCtrTime] ~first scan start, +1 last scan warp end, +2 watermark at
+// the end, +3 last gather warp exit.
+constexpr unsigned kCtrTime = 56;
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void diag_time(const ScanArgs& A, unsigned slot) {
+  if (!(A.plan.diag & 2048)) return;
+  const uint64_t t = global_ns();
+  atomicMax(A.counters + kCtrTime + slot, static_cast<unsigned long long>(slot == 0 ? ~t : t));
+}
+
 // A scanning warp leaves the kernel: its candidate count joins the counters.
 __device__ __forceinline__ void scan_exit(const ScanArgs& A, unsigned long long cands, int lane) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) cands += __shfl_xor_sync(kFull, cands, o);
   if (lane == 0 && cands) atomicAdd(A.counters + kCtrCands, cands);
+  if (lane == 0) diag_time(A, 1);
 }
 
 // Let the search's gather kernel start now (programmatic dependent launch):
 // its one-warp CTAs run beside the scan on the registers a 15-warp CTA
 // leaves free, and place slices while the scan goes on.
-__device__ __forceinline__ void allow_gather() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void allow_gather(const ScanArgs& A) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0) diag_time(A, 0);
+}
 
 // Watermark advance (one gather warp at a time, under the advance lock):
 // lane l takes the 32 groups W + 32 l ... W + 32 l + 31, so the run of
@@ -363,6 +383,7 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
             }
           }
         }
+        if (lane == 0) diag_time(A, 2);
         if (lane == 0) {  // the next launch of the search needs the lock
           fence_release();
           atomicExch(lock, 0ull);

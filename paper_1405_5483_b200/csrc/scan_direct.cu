@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant
   DirectDesc* desc = reinterpret_cast<DirectDesc*>(p) + static_cast<size_t>(warp) * DEPTH;
   p += size_t(nw) * DEPTH * sizeof(DirectDesc);
   uint64_t* bars = reinterpret_cast<uint64_t*>(p) + static_cast<size_t>(warp) * DEPTH;
-  allow_gather();
+  allow_gather(A);
   if (lane == 0) {
     for (int j = 0; j < DEPTH; ++j) mbar_init(bars + j, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

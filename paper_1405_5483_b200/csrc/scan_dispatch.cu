@@ -26,12 +26,18 @@ __global__ void __launch_bounds__(32, 16) mag_gather_kernel(const __grid_constan
   }
   old = __shfl_sync(kFull, old, 0);
   if (old + 1 != gridDim.x || !A.final_launch) return;
+  if (lane == 0) diag_time(A, 3);
   asm volatile("griddepcontrol.wait;" ::: "memory");
   fence_gpu();
   if (lane < 3) {
     const unsigned src = lane == 0 ? kCtrCands : (lane == 1 ? kCtrTotal : kCtrMax);
     const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + src);
     reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[1 + lane] = v;
+  }
+  if ((A.plan.diag & 2048) && lane < 4) {  // diagnostics timeline, ns after the first scan CTA started
+    const uint64_t t0 = ~ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime);
+    const uint64_t t = lane == 3 ? global_ns() : ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 1 + lane);
+    reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[4 + lane] = t - t0;
   }
   for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
   __threadfence_system();

@@ -389,7 +389,7 @@ constexpr int kRollThreads = 16 * 32;
 
 template <int Q, int H>
 __global__ void __launch_bounds__(kRollThreads, 1) mag_roll_kernel(const __grid_constant__ ScanArgs A) {
-  allow_gather();
+  allow_gather(A);
   extern __shared__ __align__(128) uint8_t smem[];
   const size_t tbytes = align16(A.plan.table_bytes);
   {

@@ -819,7 +819,7 @@ struct Scanner {
 
 template <int GM, typename E, bool TSMEM, int QW, int CMP, int CK, bool A4>
 __global__ void __launch_bounds__(kMaxWarps * 32, 1) mag_scan_kernel(const __grid_constant__ ScanArgs A) {
-  allow_gather();
+  allow_gather(A);
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(A.plan, A.slot_bytes, A.ring, A.nwarps);
   Smem S;
