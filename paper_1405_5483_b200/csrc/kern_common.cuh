@@ -311,6 +311,7 @@ __device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_
 // matches; clear the group word for the next search.
 __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int lane) {
   const uint64_t x = c * kGroup + lane;
+  const unsigned long long base = c == 0 ? 0ull : ld_gpu(A.group_incl + c - 1);
   const uint32_t cnt = x < A.num_slices ? __ldcg(A.slice_count + x) : 0u;
   unsigned long long v = cnt;
 #pragma unroll
@@ -318,16 +319,28 @@ __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int la
     const unsigned long long y = __shfl_up_sync(kFull, v, o);
     if (lane >= o) v += y;
   }
-  const unsigned long long base = c == 0 ? 0ull : ld_gpu(A.group_incl + c - 1);
   const unsigned long long mine = base + v - cnt;
+  // 8 loads in flight per lane (dense searches copy ~100 MB this way)
+  constexpr int kU = 8;
   for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
     const int s = __ffs(m) - 1;
     const uint32_t n = __shfl_sync(kFull, cnt, s);
     const unsigned long long dst = __shfl_sync(kFull, mine, s);
     const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
     const uint64_t* src = A.staging + (c * kGroup + s) * A.slice_cap;
-    for (uint32_t i = lane; i < cc; i += 32)
-      if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
+    for (uint32_t i0 = 0; i0 < cc; i0 += 32 * kU) {
+      uint64_t val[kU];
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        const uint32_t i = i0 + 32 * k + lane;
+        val[k] = i < cc ? __ldcg(src + i) : 0ull;
+      }
+#pragma unroll
+      for (int k = 0; k < kU; ++k) {
+        const uint32_t i = i0 + 32 * k + lane;
+        if (i < cc && dst + i < A.out_cap) A.out[dst + i] = val[k];
+      }
+    }
   }
   // zero between searches: the group word and the nonzero slice counts
   if (cnt) A.slice_count[x] = 0;
@@ -367,9 +380,12 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
         W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
         uint32_t spins = 0;
         while (W < gend) {
-          const uint64_t W2 = advance_watermark(A, W, gend, lane);
+          bool next = false;  // the group at W complete?  (one load before a full advance)
+          if (lane == 0)
+            next = (ld_gpu(A.group_word + W) >> 40) == min(static_cast<uint64_t>(kGroup), A.num_slices - W * kGroup);
+          const uint64_t W2 = __shfl_sync(kFull, next, 0) ? advance_watermark(A, W, gend, lane) : W;
           if (W2 == W) {
-            __nanosleep(spins < 16 ? 64 : 256);
+            __nanosleep(spins < 64 ? 32 : 128);
             ++spins;
           } else {
             spins = 0;
@@ -411,7 +427,7 @@ __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
     if (progress) {
       idle = 0;
     } else {
-      __nanosleep(idle < 8 ? 100 : 400);
+      __nanosleep(idle < 16 ? 64 : 200);
       ++idle;
     }
   }
