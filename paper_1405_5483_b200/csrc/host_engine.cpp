@@ -488,7 +488,7 @@ mag_status materialize(mag_matches* m) {
   m->metrics.candidates = e->plan.sp.verify_all ? analytic_candidates(e->plan, m->n) : hc[1];
 #ifdef MAG_B200_DIAGNOSTICS
   if (std::getenv("MAG_B200_TIMELINE"))
-    std::fprintf(stderr, "timeline_ns last_scan_end=%llu watermark_end=%llu last_gather=%llu counters_out=%llu\n",
+    std::fprintf(stderr, "timeline_ns last_scan_end=%llu watermark_end=%llu last_gather_exit=%llu last_gather_start=%llu\n",
                  hc[4], hc[5], hc[6], hc[7]);
 #endif
   m->pending = false;

@@ -219,7 +219,7 @@ __device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice,
 // Diagnostics builds (MAG_B200_DIAG bit 2048): a timeline of the search in
 // spare control words, ns since the first scan CTA started (the host prints
 // it): [kCtrTime] ~first scan start, +1 last scan warp end, +2 watermark at
-// the end, +3 last gather warp exit.
+// the end, +3 last gather warp exit, +4 last gather warp start.
 constexpr unsigned kCtrTime = 56;
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
@@ -320,26 +320,43 @@ __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int la
     if (lane >= o) v += y;
   }
   const unsigned long long mine = base + v - cnt;
-  // 8 loads in flight per lane (dense searches copy ~100 MB this way)
-  constexpr int kU = 8;
-  for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
-    const int s = __ffs(m) - 1;
-    const uint32_t n = __shfl_sync(kFull, cnt, s);
-    const unsigned long long dst = __shfl_sync(kFull, mine, s);
-    const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
-    const uint64_t* src = A.staging + (c * kGroup + s) * A.slice_cap;
-    for (uint32_t i0 = 0; i0 < cc; i0 += 32 * kU) {
+  constexpr int kU = 8;  // loads in flight per lane
+  if (!__any_sync(kFull, cnt > A.slice_cap)) {
+    // the group's matches as one flat run: element e belongs to the last
+    // slice whose exclusive prefix is <= e (binary search over the lanes)
+    const uint32_t excl = static_cast<uint32_t>(v) - cnt;
+    const uint32_t tot = static_cast<uint32_t>(__shfl_sync(kFull, v, 31));
+    for (uint32_t e0 = 0; e0 < tot; e0 += 32 * kU) {
       uint64_t val[kU];
 #pragma unroll
       for (int k = 0; k < kU; ++k) {
-        const uint32_t i = i0 + 32 * k + lane;
-        val[k] = i < cc ? __ldcg(src + i) : 0ull;
+        const uint32_t e = e0 + 32 * k + lane;
+        int sl = 0;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+          const uint32_t t = __shfl_sync(kFull, excl, sl + step);
+          if (t <= e) sl += step;
+        }
+        const uint32_t off = e - __shfl_sync(kFull, excl, sl);
+        val[k] = e < tot ? __ldcg(A.staging + (c * kGroup + sl) * A.slice_cap + off) : 0ull;
       }
 #pragma unroll
       for (int k = 0; k < kU; ++k) {
-        const uint32_t i = i0 + 32 * k + lane;
-        if (i < cc && dst + i < A.out_cap) A.out[dst + i] = val[k];
+        const uint32_t e = e0 + 32 * k + lane;
+        if (e < tot && base + e < A.out_cap) A.out[base + e] = val[k];
       }
+    }
+  } else {
+    // a slice overflowed its staging (the host searches again with a larger
+    // capacity): copy what fits, slice by slice
+    for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
+      const int sl = __ffs(m) - 1;
+      const uint32_t n = __shfl_sync(kFull, cnt, sl);
+      const unsigned long long dst = __shfl_sync(kFull, mine, sl);
+      const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
+      const uint64_t* src = A.staging + (c * kGroup + sl) * A.slice_cap;
+      for (uint32_t i = lane; i < cc; i += 32)
+        if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
     }
   }
   // zero between searches: the group word and the nonzero slice counts
@@ -355,6 +372,7 @@ __device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int la
 // the gather only waits for slices the scan's running warps have claimed, so
 // nothing can deadlock whether or not the two grids are co-resident.
 __device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
+  if (lane == 0) diag_time(A, 4);
   if (A.plan.diag & 256) return;  // diagnostics: no gather warp
   unsigned long long* lock = A.counters + kCtrLock;
   const uint64_t gbeg = A.slice_begin / kGroup;

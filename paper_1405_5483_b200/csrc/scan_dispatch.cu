@@ -36,7 +36,8 @@ __global__ void __launch_bounds__(32, 16) mag_gather_kernel(const __grid_constan
   }
   if ((A.plan.diag & 2048) && lane < 4) {  // diagnostics timeline, ns after the first scan CTA started
     const uint64_t t0 = ~ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime);
-    const uint64_t t = lane == 3 ? global_ns() : ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 1 + lane);
+    const uint64_t t = lane == 3 ? ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 4)
+                                 : ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 1 + lane);
     reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[4 + lane] = t - t0;
   }
   for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
