@@ -70,13 +70,14 @@ struct DirectScanner {
   unsigned long long p_t;
   uint32_t p_left;
   bool p_done;
-  unsigned long long tk;  // lane 0: the next slice ticket, claimed one slice ahead
+  unsigned long long tk;  // lane 0: the next slice ticket, claimed while staging the slice's last step
+  bool tk_valid;
   uint64_t pol;  // L2 evict-first policy of the text stream (created once)
 
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
-        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), tk(0), pol(policy_evict_first()) {
+        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), tk(0), tk_valid(false), pol(policy_evict_first()) {
     for (int i = 0; i < kPer; ++i) pend_w[i] = pend_k[i] = 0;
     pend_pos = 0;
   }
@@ -92,11 +93,11 @@ struct DirectScanner {
     uint32_t slice = 0;
     bool first = false;
     while (!p_done && p_left == 0) {
-      // the ticket was claimed a slice ago (its round trip is long done);
-      // claim the next one now.  A warp stops at its first ticket past the
-      // end, so the one it holds then is past the end too: none is lost.
+      // the ticket was claimed when the previous slice's last step was
+      // staged (a step of work hides its round trip)
+      if (!tk_valid && lane == 0) tk = atomicAdd(A.ticket, 1ull);
+      tk_valid = false;
       unsigned long long x = __shfl_sync(kFull, tk, 0) + A.slice_begin;
-      if (lane == 0) tk = atomicAdd(A.ticket, 1ull);
       if (x >= A.slice_end) {
         p_done = true;
         break;
@@ -137,6 +138,10 @@ struct DirectScanner {
       const uint32_t lim = p_left < kStep ? p_left : kStep;
       p_t += lim;
       p_left -= lim;
+      if (p_left == 0) {  // the slice's last step is staged: claim the next slice now
+        if (lane == 0) tk = atomicAdd(A.ticket, 1ull);
+        tk_valid = true;
+      }
     }
   }
 
@@ -251,7 +256,6 @@ struct DirectScanner {
   // Stage the first DEPTH steps (before the CTA loads its table, so the
   // first text bytes are in flight during the table copy).
   __device__ void start() {
-    if (lane == 0) tk = atomicAdd(A.ticket, 1ull);
 #pragma unroll 1
     for (int j = 0; j < DEPTH; ++j) produce(j);
     __syncwarp();
