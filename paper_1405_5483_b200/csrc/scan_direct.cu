@@ -70,14 +70,12 @@ struct DirectScanner {
   unsigned long long p_t;
   uint32_t p_left;
   bool p_done;
-  unsigned long long tk;  // lane 0: the next slice ticket, claimed while staging the slice's last step
-  bool tk_valid;
   uint64_t pol;  // L2 evict-first policy of the text stream (created once)
 
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
-        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), tk(0), tk_valid(false), pol(policy_evict_first()) {
+        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
     for (int i = 0; i < kPer; ++i) pend_w[i] = pend_k[i] = 0;
     pend_pos = 0;
   }
@@ -93,11 +91,9 @@ struct DirectScanner {
     uint32_t slice = 0;
     bool first = false;
     while (!p_done && p_left == 0) {
-      // the ticket was claimed when the previous slice's last step was
-      // staged (a step of work hides its round trip)
-      if (!tk_valid && lane == 0) tk = atomicAdd(A.ticket, 1ull);
-      tk_valid = false;
-      unsigned long long x = __shfl_sync(kFull, tk, 0) + A.slice_begin;
+      unsigned long long x = 0;
+      if (lane == 0) x = atomicAdd(A.ticket, 1ull);
+      x = __shfl_sync(kFull, x, 0) + A.slice_begin;
       if (x >= A.slice_end) {
         p_done = true;
         break;
@@ -138,10 +134,6 @@ struct DirectScanner {
       const uint32_t lim = p_left < kStep ? p_left : kStep;
       p_t += lim;
       p_left -= lim;
-      if (p_left == 0) {  // the slice's last step is staged: claim the next slice now
-        if (lane == 0) tk = atomicAdd(A.ticket, 1ull);
-        tk_valid = true;
-      }
     }
   }
 
