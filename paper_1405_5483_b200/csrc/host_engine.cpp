@@ -238,7 +238,7 @@ constexpr size_t kCounters = 8;
 constexpr size_t kCtrlWords = kCtrWords;
 
 struct SearchGeometry {
-  uint64_t samples, slice_samples, tail_samples, big_slices, num_slices, slice_cap;
+  uint64_t samples, slice_samples, num_slices, slice_cap;
   uint32_t bps;  // text bytes per sample
 };
 
@@ -268,19 +268,7 @@ SearchGeometry geometry(const mag_engine* e, uint64_t n, uint64_t cap_override) 
   g.samples = filter_reads(P, n);
   g.bps = static_cast<uint32_t>(bytes_per_sample(P));
   g.slice_samples = slice_samples_for(e, g.samples);
-  // The last wave of the grid runs tail slices 8x finer (about one big slice
-  // per scanning warp), so the warps run out of work together.
-  const uint64_t unit = step_unit(P);
-  g.tail_samples = std::min<uint64_t>(g.slice_samples,
-                                      std::max<uint64_t>(unit, (g.slice_samples / 8 + unit - 1) / unit * unit));
-  uint64_t tail = std::min<uint64_t>(g.samples / 2, static_cast<uint64_t>(e->sm_count) * P.nwarps * g.slice_samples);
-#ifdef MAG_B200_DIAGNOSTICS
-  if (const char* d = std::getenv("MAG_B200_DIAG"))
-    if (std::atoi(d) & 1024) tail = 0;  // profiling: uniform slices
-#endif
-  g.big_slices = g.samples > tail ? (g.samples - tail) / g.slice_samples : 0;
-  const uint64_t rest = g.samples - g.big_slices * g.slice_samples;
-  g.num_slices = g.big_slices + (rest + g.tail_samples - 1) / g.tail_samples;
+  g.num_slices = (g.samples + g.slice_samples - 1) / g.slice_samples;
   if (cap_override) {
     g.slice_cap = cap_override;
   } else {
@@ -303,8 +291,6 @@ ScanArgs geometry_args(const SearchGeometry& g) {
   ScanArgs a{};
   a.samples = g.samples;
   a.slice_samples = g.slice_samples;
-  a.big_slices = g.big_slices;
-  a.tail_samples = g.tail_samples;
   a.num_slices = g.num_slices;
   return a;
 }

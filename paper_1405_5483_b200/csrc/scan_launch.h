@@ -10,9 +10,7 @@ namespace magb {
 // Everything one scan launch needs.  Device pointers only.
 //
 // Work decomposition: the filter's samples t in [0, samples) are cut into
-// big_slices slices of slice_samples, then tail slices of tail_samples
-// (finer, so the grid's warps run out of work together).  A slice is owned
-// by one warp (dynamic ticket)
+// slices of slice_samples.  A slice is owned by one warp (dynamic ticket)
 // and produces the matches of exactly the candidate windows its samples
 // raise, in (offset, pattern) order, into staging + slice * slice_cap.  A
 // slice is streamed through the warp's ring of shared-memory slots in chunks
@@ -50,8 +48,6 @@ struct ScanArgs {
   uint32_t zero;                // always 0; opaque to the compiler (orders slot reads before TMA refills)
   uint64_t samples;             // T: floor(n_q/k) strided, n-q+1 overlapping, n verify-all
   uint64_t slice_samples;       // multiple of chunk_samples
-  uint64_t big_slices;          // slices [0, big_slices) are big, the rest tail slices
-  uint64_t tail_samples;        // tail slices: multiple of chunk_samples, <= slice_samples
   uint32_t chunk_samples;       // samples per chunk (iterations * advance)
   uint32_t back;                // staged bytes after the last gram (pattern reach)
   uint32_t full_bytes;          // staged bytes of an interior chunk (multiple of 16)
@@ -79,12 +75,9 @@ struct ScanArgs {
 
 // Slice geometry (host and device).
 constexpr unsigned kGroup = 32;  // slices per gather group
-MAG_HD uint64_t slice_t0(const ScanArgs& a, uint64_t x) {
-  return x < a.big_slices ? x * a.slice_samples
-                          : a.big_slices * a.slice_samples + (x - a.big_slices) * a.tail_samples;
-}
+MAG_HD uint64_t slice_t0(const ScanArgs& a, uint64_t x) { return x * a.slice_samples; }
 MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
-  const uint64_t t = slice_t0(a, x) + (x < a.big_slices ? a.slice_samples : a.tail_samples);
+  const uint64_t t = (x + 1) * a.slice_samples;
   return t < a.samples ? t : a.samples;
 }
 
