@@ -65,8 +65,7 @@ struct Workspace {
   uint32_t parity = 0;
   bool dirty = false;
   uint32_t* slice_count = nullptr;     // per slice: match count
-  uint64_t* group_word = nullptr;      // per 32-slice group: slices done << 40 | count (zero between searches)
-  uint64_t* group_incl = nullptr;      // per group: inclusive prefix of counts
+  unsigned long long* group_sum = nullptr;  // two halves (parity) of per-group match counts
   size_t slices_cap = 0;
   uint64_t* staging = nullptr;         // num_slices * slice_cap staged matches
   uint64_t* out = nullptr;             // sorted matches (same capacity)
@@ -86,8 +85,7 @@ struct Workspace {
     cudaSetDevice(device);
     if (ctrl) cudaFree(ctrl);
     if (slice_count) cudaFree(slice_count);
-    if (group_word) cudaFree(group_word);
-    if (group_incl) cudaFree(group_incl);
+    if (group_sum) cudaFree(group_sum);
     if (staging) cudaFree(staging);
     if (out) cudaFree(out);
     if (h_ctr) cudaFreeHost(h_ctr);
@@ -322,24 +320,20 @@ mag_status ensure_ws(Workspace* w, const SearchGeometry& g, cudaStream_t st) {
   }
   if (w->dirty) {  // new, or a search failed half-way: control words and group words from zero
     MAG_CUDA(cudaMemsetAsync(w->ctrl, 0, 2 * kCtrlWords * sizeof(unsigned long long), st));
-    if (w->group_word) MAG_CUDA(cudaMemsetAsync(w->group_word, 0, w->slices_cap / kGroup * sizeof(uint64_t), st));
-    if (w->slice_count) MAG_CUDA(cudaMemsetAsync(w->slice_count, 0, w->slices_cap * sizeof(uint32_t), st));
+    if (w->group_sum) MAG_CUDA(cudaMemsetAsync(w->group_sum, 0, 2 * w->slices_cap / kGroup * sizeof(uint64_t), st));
     w->parity = 0;
     w->dirty = false;
   }
   if (w->slices_cap < std::max<uint64_t>(1, g.num_slices)) {
     if (w->slice_count) MAG_CUDA(cudaFree(w->slice_count));
-    if (w->group_word) MAG_CUDA(cudaFree(w->group_word));
-    if (w->group_incl) MAG_CUDA(cudaFree(w->group_incl));
+    if (w->group_sum) MAG_CUDA(cudaFree(w->group_sum));
     w->slice_count = nullptr;
-    w->group_word = w->group_incl = nullptr;
+    w->group_sum = nullptr;
     w->slices_cap = 0;
     const size_t cap = (std::max<uint64_t>(1, g.num_slices) + kGroup - 1) / kGroup * kGroup;
     MAG_CUDA(cudaMalloc(&w->slice_count, cap * sizeof(uint32_t)));
-    MAG_CUDA(cudaMalloc(&w->group_word, cap / kGroup * sizeof(uint64_t)));
-    MAG_CUDA(cudaMalloc(&w->group_incl, cap / kGroup * sizeof(uint64_t)));
-    MAG_CUDA(cudaMemsetAsync(w->group_word, 0, cap / kGroup * sizeof(uint64_t), st));
-    MAG_CUDA(cudaMemsetAsync(w->slice_count, 0, cap * sizeof(uint32_t), st));
+    MAG_CUDA(cudaMalloc(&w->group_sum, 2 * cap / kGroup * sizeof(uint64_t)));
+    MAG_CUDA(cudaMemsetAsync(w->group_sum, 0, 2 * cap / kGroup * sizeof(uint64_t), st));
     w->slices_cap = cap;
   }
   const size_t cap = std::max<size_t>(1, g.num_slices * g.slice_cap);
@@ -362,8 +356,9 @@ struct SliceRange {
 
 // Enqueue one complete search over device text: the fused kernel over the
 // slice ranges (one launch per range, each after its range's wait event);
-// the final launch's last warp leaves the counters in the mapped host copy
-// and clears the next search's control words; record ws->done.  All on `st`.
+// after the final launch, the finish grid places the matches in order,
+// leaves the counters in the mapped host copy and clears the next search's
+// control words; record ws->done.  All on `st`.
 mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_text, uint64_t n,
                           const uint32_t* d_codes, cudaStream_t st,
                           const std::vector<SliceRange>& ranges, uint64_t cap_override = 0) {
@@ -407,8 +402,9 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
   a.staging = w->staging;
   a.slice_cap = static_cast<uint32_t>(std::min<uint64_t>(g.slice_cap, 0xfffffff0u));
   a.slice_count = w->slice_count;
-  a.group_word = w->group_word;
-  a.group_incl = w->group_incl;
+  a.group_sum_words = w->slices_cap / kGroup;
+  a.group_sum = w->group_sum + w->parity * a.group_sum_words;
+  a.group_sum_next = w->group_sum + (w->parity ^ 1u) * a.group_sum_words;
   a.out = w->out;
   a.out_cap = w->out_cap;
   a.counters = counters;
@@ -426,12 +422,13 @@ mag_status enqueue_search(const mag_engine* e, Workspace* w, const uint8_t* d_te
     a.slice_begin = begin;
     a.slice_end = end;
     a.ticket = counters + kCtrLaunch + kCtrPerLaunch * li;
-    a.exits = a.ticket + 16;
-    a.copy_cursor = a.ticket + 32;
+    a.exits = counters + kCtrExits;
     ++li;
     const uint64_t ctas = std::max<uint64_t>(1, (end - begin + P.nwarps - 1) / P.nwarps);
     const int grid = static_cast<int>(std::min<uint64_t>(ctas, static_cast<uint64_t>(e->sm_count)));
     a.final_launch = final_launch ? 1u : 0u;
+    a.finish_grid = static_cast<uint32_t>(std::max<uint64_t>(
+        1, std::min<uint64_t>((g.num_slices + kGroup - 1) / kGroup, static_cast<uint64_t>(e->sm_count))));
     MAG_CUDA(timed_launch(a, st, grid));
     return MAG_OK;
   };
@@ -902,9 +899,7 @@ MAG_API mag_status mag_search(const mag_engine* e, const uint8_t* text, size_t l
       }
       MAG_CUDA(cudaEventRecord(w->chunk_ev[ci], w->copy_stream));
       // slices whose bytes (plus the pattern reach) have fully arrived
-      // (launches end on gather-group boundaries: a group never spans two)
-      const uint64_t ready =
-          copied == len ? slices : (copied > reach ? slices_ending_by(sg, copied - reach) / kGroup * kGroup : 0);
+      const uint64_t ready = copied == len ? slices : (copied > reach ? slices_ending_by(sg, copied - reach) : 0);
       ranges.push_back(SliceRange{slices_done, ready, w->chunk_ev[ci]});
       slices_done = std::max(slices_done, ready);
       ++ci;

@@ -1,7 +1,7 @@
 // Device helpers shared by the scan kernels (scan_staged.cuh, scan_direct.cu,
 // scan_roll.cu): PTX wrappers (mbarrier, 1-D TMA bulk copies, L2 policy),
 // warp scans, exact compares against the text, the window-key bucket walk,
-// and the in-kernel ordered gather (slice publication, gather warp, exit).
+// and the slice publication the finish grid reads (scan_dispatch.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -60,22 +60,6 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane) {
     if (lane >= o) x += y;
   }
   return x - v;
-}
-
-// Coherent (L2) 64-bit load/store for words other warps write in this launch.
-__device__ __forceinline__ uint64_t ld_gpu(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-// Fences at GPU scope.  An acquire (fence.acq_rel, ld.acquire) invalidates the
-// SM's whole L1 (CCTL.IVALL), which the scanning warps' screen and pattern
-// loads rely on: the scanning warps only ever release (MEMBAR, no IVALL);
-// the gather warps acquire once per lock or copy claim.
-__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
-__device__ __forceinline__ void st_gpu(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Exact compare of pattern pid against text[a, a + len) in global memory:
@@ -194,42 +178,35 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
   return fill;
 }
 
-// ------------------------------------------------------------ ordered gather
-// Slice end (whole warp): the slice's staged matches and its count become
-// visible before its group word says "one more slice done".  slice_count is
-// zero between searches (the copier clears it), so an empty slice stores
-// nothing and needs no fence (a fence waits ~1 us for the store
-// acknowledgements; most slices of a sparse search are empty).  The largest
-// slice count (staging overflow check, learned density) is a fire-and-forget
-// reduction.
-__device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
-  if (A.plan.diag & 512) return;  // diagnostics: no publication (no gather)
-  if (count) {
-    if (lane == 0) A.slice_count[slice] = count;
-    fence_release();  // every lane's staged matches (and the count) before the group word
-  }
-  __syncwarp();
-  if (lane == 0) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(A.group_word + slice / kGroup), (1ull << 40) | count);
-    if (count) atomicMax(A.counters + kCtrMax, static_cast<unsigned long long>(count));
-  }
-  __syncwarp();
-}
-
+// ------------------------------------------------------------ ordered output
 // Diagnostics builds (MAG_B200_DIAG bit 2048): a timeline of the search in
-// spare control words, ns since the first scan CTA started (the host prints
-// it): [kCtrTime] ~first scan start, +1 last scan warp end, +2 watermark at
-// the end, +3 last gather warp exit, +4 last gather warp start.
+// spare control words, ns after the first scan CTA started (the host prints
+// it): [kCtrTime] ~first scan start, +1 last scan warp end, +2 first finish
+// CTA past its wait, +3 last finish CTA done.
 constexpr unsigned kCtrTime = 56;
 __device__ __forceinline__ uint64_t global_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void diag_time(const ScanArgs& A, unsigned slot) {
+__device__ __forceinline__ void diag_time(const ScanArgs& A, unsigned slot, bool first = false) {
   if (!(A.plan.diag & 2048)) return;
   const uint64_t t = global_ns();
-  atomicMax(A.counters + kCtrTime + slot, static_cast<unsigned long long>(slot == 0 ? ~t : t));
+  atomicMax(A.counters + kCtrTime + slot, static_cast<unsigned long long>(first ? ~t : t));
+}
+
+// Slice end (whole warp): the count, and for a nonzero count one atomic into
+// its group's sum and one into the largest-slice counter (staging overflow
+// check, learned density).  No fence: the finish grid reads them after the
+// scan grid has completed.
+__device__ __forceinline__ void publish_slice(const ScanArgs& A, uint64_t slice, uint32_t count, int lane) {
+  if (lane == 0) {
+    A.slice_count[slice] = count;
+    if (count) {
+      atomicAdd(A.group_sum + slice / kGroup, static_cast<unsigned long long>(count));
+      atomicMax(A.counters + kCtrMax, static_cast<unsigned long long>(count));
+    }
+  }
 }
 
 // A scanning warp leaves the kernel: its candidate count joins the counters.
@@ -240,215 +217,11 @@ __device__ __forceinline__ void scan_exit(const ScanArgs& A, unsigned long long 
   if (lane == 0) diag_time(A, 1);
 }
 
-// Let the search's gather kernel start now (programmatic dependent launch):
-// its one-warp CTAs run beside the scan on the registers a 15-warp CTA
-// leaves free, and place slices while the scan goes on.
+// Let the finish grid launch now (programmatic dependent launch): its CTAs
+// take SMs as the scan's CTAs leave and wait there for the scan to complete.
 __device__ __forceinline__ void allow_gather(const ScanArgs& A) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (threadIdx.x == 0) diag_time(A, 0);
-}
-
-// Watermark advance (one gather warp at a time, under the advance lock):
-// lane l takes the 32 groups W + 32 l ... W + 32 l + 31, so the run of
-// complete groups right above W (up to 1024 groups = 32768 slices) is found
-// and prefix-summed with per-lane serial sums and one warp scan; the
-// inclusive prefix counts go to group_incl[] and the new watermark is stored
-// after them.  Returns the new W (groups).
-__device__ __forceinline__ uint64_t advance_watermark(const ScanArgs& A, uint64_t W, uint64_t gend, int lane) {
-  constexpr int kPer = 32;
-  const uint64_t g0 = W + static_cast<uint64_t>(kPer) * lane;
-  uint64_t wd[kPer];
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) wd[i] = g0 + i < gend ? ld_gpu(A.group_word + g0 + i) : 0ull;
-  const unsigned long long base = W == 0 ? 0ull : ld_gpu(A.group_incl + W - 1);
-  int lead = kPer;
-#pragma unroll
-  for (int i = kPer - 1; i >= 0; --i) {
-    const uint64_t g = g0 + i;
-    const uint64_t want = g < gend ? min(static_cast<uint64_t>(kGroup), A.num_slices - g * kGroup) : ~0ull;
-    if ((wd[i] >> 40) != want) lead = i;
-  }
-  unsigned long long sum = 0;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i)
-    if (i < lead) sum += wd[i] & ((1ull << 40) - 1);
-  const unsigned partial = __ballot_sync(kFull, lead < kPer);
-  const int stop = partial ? __ffs(partial) - 1 : 32;
-  if (lane > stop) {
-    lead = 0;
-    sum = 0;
-  }
-  const uint64_t j = static_cast<uint64_t>(kPer) * stop + (stop < 32 ? __shfl_sync(kFull, lead, stop) : 0);
-  if (j == 0) return W;
-  unsigned long long v = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(kFull, v, o);
-    if (lane >= o) v += y;
-  }
-  const unsigned long long end = base + __shfl_sync(kFull, v, 31);
-  unsigned long long run = base + v - sum;
-#pragma unroll
-  for (int i = 0; i < kPer; ++i)
-    if (i < lead) {
-      run += wd[i] & ((1ull << 40) - 1);
-      st_gpu(A.group_incl + g0 + i, run);
-    }
-  W += j;
-  fence_release();  // every lane's prefix stores before the new watermark
-  __syncwarp();
-  if (lane == 0) {
-    if (W * kGroup >= A.num_slices) st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrTotal, end);
-    fence_release();
-    st_gpu(reinterpret_cast<uint64_t*>(A.counters) + kCtrWatermark, W);
-  }
-  __syncwarp();
-  return W;
-}
-
-// Place group c (below the watermark): its slices' offsets are the group's
-// exclusive prefix plus a warp scan of their counts; copy their staged
-// matches; clear the group word for the next search.
-__device__ __forceinline__ void copy_group(const ScanArgs& A, uint64_t c, int lane) {
-  const uint64_t x = c * kGroup + lane;
-  const unsigned long long base = c == 0 ? 0ull : ld_gpu(A.group_incl + c - 1);
-  const uint32_t cnt = x < A.num_slices ? __ldcg(A.slice_count + x) : 0u;
-  unsigned long long v = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const unsigned long long y = __shfl_up_sync(kFull, v, o);
-    if (lane >= o) v += y;
-  }
-  const unsigned long long mine = base + v - cnt;
-  constexpr int kU = 8;  // loads in flight per lane
-  if (!__any_sync(kFull, cnt > A.slice_cap)) {
-    // the group's matches as one flat run: element e belongs to the last
-    // slice whose exclusive prefix is <= e (binary search over the lanes)
-    const uint32_t excl = static_cast<uint32_t>(v) - cnt;
-    const uint32_t tot = static_cast<uint32_t>(__shfl_sync(kFull, v, 31));
-    for (uint32_t e0 = 0; e0 < tot; e0 += 32 * kU) {
-      uint64_t val[kU];
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t e = e0 + 32 * k + lane;
-        int sl = 0;
-#pragma unroll
-        for (int step = 16; step; step >>= 1) {
-          const uint32_t t = __shfl_sync(kFull, excl, sl + step);
-          if (t <= e) sl += step;
-        }
-        const uint32_t off = e - __shfl_sync(kFull, excl, sl);
-        val[k] = e < tot ? __ldcg(A.staging + (c * kGroup + sl) * A.slice_cap + off) : 0ull;
-      }
-#pragma unroll
-      for (int k = 0; k < kU; ++k) {
-        const uint32_t e = e0 + 32 * k + lane;
-        if (e < tot && base + e < A.out_cap) A.out[base + e] = val[k];
-      }
-    }
-  } else {
-    // a slice overflowed its staging (the host searches again with a larger
-    // capacity): copy what fits, slice by slice
-    for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
-      const int sl = __ffs(m) - 1;
-      const uint32_t n = __shfl_sync(kFull, cnt, sl);
-      const unsigned long long dst = __shfl_sync(kFull, mine, sl);
-      const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
-      const uint64_t* src = A.staging + (c * kGroup + sl) * A.slice_cap;
-      for (uint32_t i = lane; i < cc; i += 32)
-        if (dst + i < A.out_cap) A.out[dst + i] = __ldcg(src + i);
-    }
-  }
-  // zero between searches: the group word and the nonzero slice counts
-  if (cnt) A.slice_count[x] = 0;
-  if (lane == 0) st_gpu(A.group_word + c, 0ull);
-}
-
-// A gather warp (scan_dispatch.cu mag_gather_kernel: one per CTA, grid
-// beside the scan).  Two jobs: advancing the watermark (the warp that takes
-// the advance lock keeps advancing while groups complete), and copying: each
-// gather warp claims one group at a time (a cursor per launch) and places it
-// once the watermark has passed it.  The scan never waits for the gather, and
-// the gather only waits for slices the scan's running warps have claimed, so
-// nothing can deadlock whether or not the two grids are co-resident.
-__device__ __noinline__ void gather_warp_run(const ScanArgs& A, int lane) {
-  if (lane == 0) diag_time(A, 4);
-  if (A.plan.diag & 256) return;  // diagnostics: no gather warp
-  unsigned long long* lock = A.counters + kCtrLock;
-  const uint64_t gbeg = A.slice_begin / kGroup;
-  const uint64_t gend = (A.slice_end + kGroup - 1) / kGroup;  // launches end on group boundaries
-  uint64_t claim = ~0ull;
-  bool claims_done = false, advancer = false;
-  uint32_t idle = 0;
-  while (true) {
-    uint64_t W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
-    bool progress = false;
-    bool ready = false;  // the lock is only tried when the group at the watermark is complete
-    if (lane == 0 && !advancer && W < gend)
-      ready = (ld_gpu(A.group_word + W) >> 40) == min(static_cast<uint64_t>(kGroup), A.num_slices - W * kGroup);
-    if (!advancer && __shfl_sync(kFull, ready, 0)) {
-      unsigned long long got = 1;
-      if (lane == 0) got = atomicCAS(lock, 0ull, 1ull);
-      got = __shfl_sync(kFull, got, 0);
-      if (got == 0) {
-        // this warp is the advancer until the launch's last group: it polls
-        // the group words itself (one warp spinning on one SM), so the
-        // watermark follows the scan by about one poll
-        fence_gpu();
-        W = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrWatermark);
-        uint32_t spins = 0;
-        while (W < gend) {
-          bool next = false;  // the group at W complete?  (one load before a full advance)
-          if (lane == 0)
-            next = (ld_gpu(A.group_word + W) >> 40) == min(static_cast<uint64_t>(kGroup), A.num_slices - W * kGroup);
-          const uint64_t W2 = __shfl_sync(kFull, next, 0) ? advance_watermark(A, W, gend, lane) : W;
-          if (W2 == W) {
-            __nanosleep(spins < 64 ? 32 : 128);
-            ++spins;
-          } else {
-            spins = 0;
-            progress = true;
-            W = W2;
-            // place a claimed group as soon as the watermark passes it
-            if (claim != ~0ull && claim < W) {
-              fence_gpu();
-              copy_group(A, claim, lane);
-              claim = ~0ull;
-            }
-          }
-        }
-        if (lane == 0) diag_time(A, 2);
-        if (lane == 0) {  // the next launch of the search needs the lock
-          fence_release();
-          atomicExch(lock, 0ull);
-        }
-      } else {
-        advancer = true;  // someone else holds the advance for this launch
-      }
-    }
-    if (!claims_done && claim == ~0ull) {
-      unsigned long long c = 0;
-      if (lane == 0) c = atomicAdd(A.copy_cursor, 1ull);
-      c = __shfl_sync(kFull, c, 0) + gbeg;
-      if (c >= gend)
-        claims_done = true;
-      else
-        claim = c;
-    }
-    if (claim != ~0ull && claim < W) {
-      fence_gpu();
-      copy_group(A, claim, lane);
-      claim = ~0ull;
-      progress = true;
-    }
-    if (claims_done && claim == ~0ull && W >= gend) break;
-    if (progress) {
-      idle = 0;
-    } else {
-      __nanosleep(idle < 16 ? 64 : 200);
-      ++idle;
-    }
-  }
+  if (threadIdx.x == 0) diag_time(A, 0, true);
 }
 
 }  // namespace

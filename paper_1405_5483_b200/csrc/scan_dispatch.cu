@@ -11,36 +11,135 @@ namespace {
 
 std::atomic<unsigned long long> g_launches{0};
 
-// The search's gather grid: one warp per CTA, launched as a programmatic
-// dependent of the scan so it runs beside it (kern_common.cuh
-// gather_warp_run).  The last gather warp of the final launch waits for the
-// scan grid to complete (its candidate counts), then publishes the counters
-// to the mapped host words and clears the next search's control words.
-__global__ void __launch_bounds__(32, 16) mag_gather_kernel(const __grid_constant__ ScanArgs A) {
-  const int lane = threadIdx.x & 31;
-  gather_warp_run(A, lane);
-  unsigned long long old = 0;
-  if (lane == 0) {
-    fence_release();
-    old = atomicAdd(A.exits, 1ull);
-  }
-  old = __shfl_sync(kFull, old, 0);
-  if (old + 1 != gridDim.x || !A.final_launch) return;
-  if (lane == 0) diag_time(A, 3);
+// The finish grid: places every slice's staged matches at its final
+// offset once the search's scan grid has completed (griddepcontrol.wait: it
+// is launched as the scan's programmatic dependent, so its CTAs are resident
+// and waiting as the scan's CTAs leave).  CTA b owns groups [g0, g1): the
+// sum of the group sums before g0 (a coalesced pass over at most a few
+// thousand words) and a block scan of its own give each group's base; a warp
+// per group scans the group's 32 slice counts and copies the group's matches
+// as one flat run, 8 loads in flight per lane.  The last CTA out publishes
+// the counters and clears the next search's control words.
+constexpr int kFinishThreads = 512;
+__global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid_constant__ ScanArgs A) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  fence_gpu();
-  if (lane < 3) {
-    const unsigned src = lane == 0 ? kCtrCands : (lane == 1 ? kCtrTotal : kCtrMax);
-    const unsigned long long v = ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + src);
-    reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[1 + lane] = v;
+  if (threadIdx.x == 0) diag_time(A, 2, true);
+  __shared__ unsigned long long red[kFinishThreads / 32];
+  __shared__ unsigned long long s_base[kFinishThreads];  // inclusive sums of the owned groups (this chunk)
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int kW = kFinishThreads / 32;
+  const uint64_t G = (A.num_slices + kGroup - 1) / kGroup;
+  const uint64_t g0 = blockIdx.x * G / gridDim.x, g1 = (blockIdx.x + 1) * G / gridDim.x;
+  // clear the other half of the group sums for the next search
+  for (uint64_t i = blockIdx.x * kFinishThreads + tid; i < A.group_sum_words; i += uint64_t(gridDim.x) * kFinishThreads)
+    A.group_sum_next[i] = 0;
+  // matches before g0
+  unsigned long long acc = 0;
+  for (uint64_t i = tid; i < g0; i += kFinishThreads) acc += A.group_sum[i];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane == 0) red[wid] = acc;
+  __syncthreads();
+  unsigned long long base = 0;
+  for (int w = 0; w < kW; ++w) base += red[w];
+  __syncthreads();
+  for (uint64_t c0 = g0; c0 < g1; c0 += kFinishThreads) {
+    // block scan of this chunk's group sums
+    const uint64_t g = c0 + tid;
+    const unsigned long long gs = g < g1 ? A.group_sum[g] : 0ull;
+    unsigned long long v = gs;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(kFull, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) red[wid] = v;
+    __syncthreads();
+    unsigned long long wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += red[w];
+    unsigned long long ctot = 0;
+    for (int w = 0; w < kW; ++w) ctot += red[w];
+    s_base[tid] = base + wbase + v - gs;  // exclusive base of group g
+    __syncthreads();
+    // a warp per group: slice counts -> offsets -> flat copy
+    const uint64_t nchunk = g1 - c0 < kFinishThreads ? g1 - c0 : kFinishThreads;
+    for (uint64_t k = wid; k < nchunk; k += kW) {
+      const uint64_t grp = c0 + k;
+      const unsigned long long gb = s_base[k];
+      const uint64_t x = grp * kGroup + lane;
+      const uint32_t cnt = x < A.num_slices ? A.slice_count[x] : 0u;
+      uint32_t u = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, u, o);
+        if (lane >= o) u += y;
+      }
+      const uint32_t excl = u - cnt, tot = __shfl_sync(kFull, u, 31);
+      if (!tot) continue;
+      constexpr int kU = 8;
+      if (!__any_sync(kFull, cnt > A.slice_cap)) {
+        // element e belongs to the last slice whose exclusive prefix is <= e
+        for (uint32_t e0 = 0; e0 < tot; e0 += 32 * kU) {
+          uint64_t val[kU];
+#pragma unroll
+          for (int j = 0; j < kU; ++j) {
+            const uint32_t e = e0 + 32 * j + lane;
+            int sl = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1) {
+              const uint32_t t = __shfl_sync(kFull, excl, sl + step);
+              if (t <= e) sl += step;
+            }
+            const uint32_t off = e - __shfl_sync(kFull, excl, sl);
+            val[j] = e < tot ? A.staging[(grp * kGroup + sl) * A.slice_cap + off] : 0ull;
+          }
+#pragma unroll
+          for (int j = 0; j < kU; ++j) {
+            const uint32_t e = e0 + 32 * j + lane;
+            if (e < tot && gb + e < A.out_cap) A.out[gb + e] = val[j];
+          }
+        }
+      } else {
+        // a slice overflowed its staging (the host searches again with a
+        // larger capacity): copy what fits, slice by slice
+        for (unsigned m = __ballot_sync(kFull, cnt != 0); m; m &= m - 1) {
+          const int sl = __ffs(m) - 1;
+          const uint32_t n = __shfl_sync(kFull, cnt, sl);
+          const unsigned long long dst = gb + __shfl_sync(kFull, excl, sl);
+          const uint32_t cc = n < A.slice_cap ? n : A.slice_cap;
+          const uint64_t* src = A.staging + (grp * kGroup + sl) * A.slice_cap;
+          for (uint32_t i = lane; i < cc; i += 32)
+            if (dst + i < A.out_cap) A.out[dst + i] = src[i];
+        }
+      }
+    }
+    base += ctot;
+    __syncthreads();
   }
-  if ((A.plan.diag & 2048) && lane < 4) {  // diagnostics timeline, ns after the first scan CTA started
-    const uint64_t t0 = ~ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime);
-    const uint64_t t = lane == 3 ? ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 4)
-                                 : ld_gpu(reinterpret_cast<const uint64_t*>(A.counters) + kCtrTime + 1 + lane);
-    reinterpret_cast<volatile unsigned long long*>(A.host_ctr)[4 + lane] = t - t0;
+  // the block of the last groups knows the total; the last CTA out publishes
+  if (blockIdx.x == gridDim.x - 1 && tid == 0) A.counters[kCtrTotal] = base;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(A.counters + kCtrExits, 1ull) + 1 == gridDim.x;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    const volatile unsigned long long* c = A.counters;
+    volatile unsigned long long* h = A.host_ctr;
+    h[1] = c[kCtrCands];
+    h[2] = c[kCtrTotal];
+    h[3] = c[kCtrMax];
   }
-  for (uint32_t i = lane; i < A.reset_words; i += 32) A.reset[i] = 0;
+  if ((A.plan.diag & 2048) && tid < 4) {  // diagnostics timeline
+    const volatile unsigned long long* c = A.counters;
+    const uint64_t t0 = ~c[kCtrTime];
+    const uint64_t t = tid == 2 ? global_ns() : (tid == 1 ? ~c[kCtrTime + 2] : c[kCtrTime + 1 + tid]);
+    A.host_ctr[4 + tid] = t - t0;
+  }
+  __syncthreads();
+  for (uint32_t i = tid; i < A.reset_words; i += kFinishThreads) A.reset[i] = 0;
   __threadfence_system();
 }
 
@@ -102,10 +201,10 @@ cudaError_t launch_scan_only(const ScanArgs& a, cudaStream_t stream, int grid) {
 
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
   cudaError_t e = launch_scan_only(a, stream, grid);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || !a.final_launch) return e;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(32);
+  cfg.gridDim = dim3(a.finish_grid);
+  cfg.blockDim = dim3(kFinishThreads);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -113,7 +212,7 @@ cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, mag_gather_kernel, a);
+  e = cudaLaunchKernelEx(&cfg, mag_finish_kernel, a);
   if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();

@@ -16,19 +16,15 @@ namespace magb {
 // slice is streamed through the warp's ring of shared-memory slots in chunks
 // of chunk_samples samples (TMA bulk copies, one mbarrier per slot).
 //
-// Ordered gather (concurrent, no second pass).  Slices form groups of 32
-// (kGroup).  At the end of a slice its owner stores the count in
-// slice_count[] and adds (1 << 40 | count) to its group's word.  A gather
-// grid of one-warp CTAs runs beside the scan (programmatic dependent launch
-// into the registers a 15-warp scan CTA leaves free): under a lock, one
-// gather warp at a time advances the watermark
-// (counters[kCtrWatermark], in groups) over complete groups, writing their
-// inclusive prefix counts into group_incl[]; every gather warp claims one
-// group at a time below the watermark, places its slices (a warp scan of
-// their counts) and copies their staged matches to out[prefix..].  The last
-// gather warp of the final launch of a search writes the counters to
-// host_ctr (mapped pinned host memory) and zeroes the next search's control
-// words.
+// Ordered output.  Slices form groups of 32 (kGroup).  At the end of a slice
+// its owner stores the count in slice_count[] and, when nonzero, adds it to
+// its group's sum (one atomic; no fence: the finish grid reads them after
+// the scan grid has completed).  The finish grid (scan_dispatch.cu), launched
+// as the scan's programmatic dependent so its CTAs are resident and waiting
+// when the scan's last CTA leaves, places every group: exclusive prefix of
+// the group sums before it, a warp scan of its slice counts, a flat copy of
+// the staged matches to out[].  Its last CTA writes the counters to host_ctr
+// (mapped pinned host memory) and zeroes the next search's control words.
 struct ScanArgs {
   ScanPlan plan;
   const uint8_t* text;          // 16-byte aligned
@@ -59,15 +55,16 @@ struct ScanArgs {
   uint64_t* staging;            // num_slices * slice_cap packed matches
   uint32_t slice_cap;           // multiple of 16 (slices never share a 128-byte line)
   uint32_t* slice_count;        // per slice: exact match count (even past slice_cap)
-  uint64_t* group_word;         // per group: completed slices << 40 | match count (zeroed after its copy)
-  uint64_t* group_incl;         // per group: inclusive prefix of counts (valid below the watermark)
+  unsigned long long* group_sum;       // per group: match count (this search's half, zero at its start)
+  unsigned long long* group_sum_next;  // the other half: zeroed by the finish grid for the next search
+  uint64_t group_sum_words;     // words per half
   uint64_t* out;                // sorted output
   uint64_t out_cap;
   unsigned long long* counters; // control words (kCtr*)
   unsigned long long* ticket;   // slice ticket of this launch (zeroed)
-  unsigned long long* exits;    // warps of this launch that have left (zeroed)
-  unsigned long long* copy_cursor;  // gather warps' copy claims of this launch (zeroed)
-  uint32_t final_launch;        // 1: the search's last launch publishes the counters
+  unsigned long long* exits;    // finish CTAs that have left (zeroed)
+  uint32_t final_launch;        // 1: the search's last launch; the finish grid follows it
+  uint32_t finish_grid;         // CTAs of the finish grid (>= 1)
   unsigned long long* host_ctr; // mapped pinned host words: [1] candidates [2] matches [3] max slice count
   unsigned long long* reset;    // zeroed by the final launch's last warp (next search's control words)
   uint32_t reset_words;
@@ -84,13 +81,12 @@ MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
 // Control words of one search (a half of the workspace's ctrl array).
 // Each group has its own 128-byte line, so the scanning warps' ticket
 // atomics never share a line with the gather warps' polls.
-constexpr unsigned kCtrWatermark = 0;  // gather watermark (groups)
-constexpr unsigned kCtrTotal = 1;      // total matches (set when the watermark reaches the end)
-constexpr unsigned kCtrLock = 16;      // watermark-advance lock
+constexpr unsigned kCtrTotal = 1;      // total matches (finish grid)
+constexpr unsigned kCtrExits = 16;     // finish CTAs that have left
 constexpr unsigned kCtrCands = 32;     // filter candidates
 constexpr unsigned kCtrMax = 48;       // largest slice count
-constexpr unsigned kCtrLaunch = 64;    // launch li: ticket at kCtrLaunch + kCtrPerLaunch * li, exits +16, copies +32
-constexpr unsigned kCtrPerLaunch = 48;
+constexpr unsigned kCtrLaunch = 64;    // launch li: slice ticket at kCtrLaunch + kCtrPerLaunch * li
+constexpr unsigned kCtrPerLaunch = 16;
 constexpr unsigned kMaxLaunches = 64;
 constexpr unsigned kCtrWords = kCtrLaunch + kCtrPerLaunch * kMaxLaunches;
 
@@ -99,9 +95,9 @@ struct LaunchShape {
   unsigned threads;
 };
 
-// Enqueues the fused filter + verify kernel (persistent, `grid` CTAs) and
-// beside it, as its programmatic dependent, the gather grid (`grid` one-warp
-// CTAs) that places the slices' matches in order.
+// Enqueues the fused filter + verify kernel (persistent, `grid` CTAs); after
+// the search's final launch, the finish grid (programmatic dependent) that
+// places the slices' matches in order and publishes the counters.
 cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid);
 
 // SMAG prepare: codes[u] = mask index of gram u, for u < n/q.
