@@ -44,7 +44,8 @@ typedef enum mag_scan_kernel {
   MAG_KERNEL_AUTO = 0,
   MAG_KERNEL_STAGED = 1, /* TMA-staged strided / overlapping machine (every plan shape) */
   MAG_KERNEL_DIRECT = 2, /* q = 16 aligned-sample stream + L2 screen (m >= 31) */
-  MAG_KERNEL_ROLL = 3    /* dense rolling-hash prefix Bloom scan (m >= 8) */
+  MAG_KERNEL_ROLL = 3,   /* dense rolling-hash prefix Bloom scan (m >= 8) */
+  MAG_KERNEL_PACK2 = 4   /* dense 2-bit exact-code scan (<= 4 pattern symbols, m >= 10) */
 } mag_scan_kernel;
 
 MAG_API void mag_options_ex_init(mag_options_ex* opts);
@@ -74,6 +75,7 @@ typedef struct mag_plan_info {
   int direct;           /* q = 16 stream kernel */
   int roll;             /* dense rolling-hash scan (every position, q-byte prefix Bloom) */
   int cluster;          /* always 0 (kept for ABI stability) */
+  int pack2;            /* dense 2-bit exact-code scan (sigma' = 4 codes, two levels) */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

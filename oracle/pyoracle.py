@@ -374,3 +374,32 @@ def roll_candidates(text, patterns, q: int, words: int, probes: int) -> int:
     for b in bits:
         ok &= ((table[w] >> b) & np.uint32(1)).astype(bool)
     return int(ok.sum())
+
+
+# ---------------------------------------------------------------- pack2 --
+# Restatement of the GPU's two-level 2-bit-code filter (a GPU plan of the
+# reference's sigma' = 4 exact q-gram codes, qgram.hpp:30-36; see
+# paper_1405_5483_b200/csrc/scan_pack2.cu): level 1 is the set of the
+# patterns' first-10-symbol codes; a position p <= n - q is a candidate when
+# its own first-10-symbol code is in that set.
+def pack2_codes(text, length: int, shift: int) -> np.ndarray:
+    """code(p) = sum_{i<length} ((t[p+i] >> shift) & 3) << 2i for p <= n - length."""
+    t = _u8(text).astype(np.uint32)
+    n = t.size - length + 1
+    if n <= 0:
+        return np.zeros(0, dtype=np.uint32)
+    s = (t >> np.uint32(shift)) & np.uint32(3)
+    c = np.zeros(n, dtype=np.uint32)
+    for i in range(length):
+        c |= s[i:i + n] << np.uint32(2 * i)
+    return c
+
+
+def pack2_candidates(text, patterns, q: int, shift: int) -> int:
+    keys = np.unique(np.array([pack2_codes(p[:10], 10, shift)[0] for p in patterns], dtype=np.uint32))
+    t = _u8(text)
+    n = t.size - q + 1
+    if n <= 0:
+        return 0
+    codes = pack2_codes(t[: n + 9], 10, shift)[:n]
+    return int(np.isin(codes, keys).sum())

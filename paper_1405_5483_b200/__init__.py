@@ -46,7 +46,7 @@ MAPPINGS = {"auto": -1, "identity": 0, "freq": 1, "balance": 2, "lowbits": 3}
 # mag_gram_mode (mag_b200.h)
 GRAM_AUTO, GRAM_EXACT, GRAM_HASHED = -1, 0, 1
 # mag_scan_kernel (mag_b200.h)
-KERNELS = {"auto": 0, "staged": 1, "direct": 2, "roll": 3}
+KERNELS = {"auto": 0, "staged": 1, "direct": 2, "roll": 3, "pack2": 4}
 
 
 class MagError(RuntimeError):
@@ -90,6 +90,7 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("warps", C.c_uint32), ("stages", C.c_uint32), ("smem_bytes", C.c_size_t),
         ("predicted_candidates_per_byte", C.c_double), ("probes", C.c_uint32),
         ("blocks", C.c_uint32), ("direct", C.c_int), ("roll", C.c_int), ("cluster", C.c_int),
+        ("pack2", C.c_int),
     ]
 
 

@@ -245,6 +245,7 @@ uint64_t bytes_per_sample(const Plan& P) {
 }
 
 uint64_t step_unit(const Plan& P) {
+  if (P.sp.pack2) return kPack2Step;
   return P.sp.roll ? kRollStep : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);
 }
 
@@ -628,7 +629,7 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     if (opts.cluster != 0 && opts.cluster != 1)
       return fail(MAG_ERR_BAD_CONFIG, "cluster must be 0 (auto) or 1 (the cluster-shared table was retired)");
     rq.kernel = opts.scan_kernel;
-    if (opts.scan_kernel < 0 || opts.scan_kernel > 3)
+    if (opts.scan_kernel < 0 || opts.scan_kernel > 4)
       return fail(MAG_ERR_BAD_CONFIG, "unknown scan kernel " + std::to_string(opts.scan_kernel));
     if (opts.base.q < 0 || opts.base.k < 0 || opts.base.sigma_prime < 0)
       return fail(MAG_ERR_BAD_CONFIG, "q, k and sigma' must be >= 0 (0 = auto)");
@@ -639,6 +640,7 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     if (ps != 0) return fail(static_cast<mag_status>(ps), err);
     build_masks(e->plan, e->pd, &e->table);
     build_pattern_table(e->plan, e->pd, &e->ptab);
+    e->plan.sp.vbits = e->ptab.vbits;
     if (opts.device == -2) {
       e->device = -2;
     } else {
@@ -720,6 +722,7 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->direct = P.sp.direct;
   out->roll = P.sp.roll;
   out->cluster = 0;
+  out->pack2 = P.sp.pack2;
   return MAG_OK;
 }
 

@@ -441,6 +441,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       uint32_t chunk = kChunkTarget;
       int direct = 0;
       int roll = 0;
+      int pack2 = 0;
+      uint32_t pack_shift = 0;
       uint32_t roll_words = 0, halo = 0, ddepth = 0, warps = 0;
       uint32_t blocks = 0;
       bool va = true;
@@ -667,6 +669,44 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         }
       }
     }
+    // pack2: the pattern alphabet has <= 4 symbols and some shift s makes
+    // b -> (b >> s) & 3 injective on it (DNA: s = 1).  It replaces the
+    // rolling-hash scan where that scan was chosen (dense pattern sets), or
+    // runs when forced (scan_kernel = 4).
+    int pack_shift = -1;
+    {
+      bool used[256] = {false};
+      for (size_t i = 0; i < pd.r; ++i)
+        for (uint32_t j = 0; j < pd.len[i]; ++j) used[pd.pattern(i)[j]] = true;
+      int distinct = 0;
+      for (int c = 0; c < 256; ++c) distinct += used[c];
+      for (int s = 0; s <= 6 && distinct <= 4 && pack_shift < 0; ++s) {
+        unsigned seen = 0;
+        bool ok = true;
+        for (int c = 0; c < 256 && ok; ++c)
+          if (used[c]) {
+            const unsigned v = 1u << ((c >> s) & 3);
+            ok = !(seen & v);
+            seen |= v;
+          }
+        if (ok) pack_shift = s;
+      }
+    }
+    const bool pack_ok = pack_shift >= 0 && m >= 10 && rq.table_bits >= 0 && rq.variant != 1 && rq.k <= 1 &&
+                         rq.stages == 0 && rq.tile_bytes == 0 && rq.q == 0;
+    if (pack_ok && (rq.kernel == 4 || (rq.kernel == 0 && best.roll))) {
+      best = Cand{};
+      best.cost = 0;
+      best.q = static_cast<unsigned>(std::min<size_t>(m, 16));
+      best.va = false;
+      best.og = 1;
+      best.pack2 = 1;
+      best.pack_shift = static_cast<uint32_t>(pack_shift);
+      best.halo = 32;
+      best.chunk = kPack2Step;
+      // level-1 candidates: keys' distinct 10-symbol prefixes over 2^20
+      best.cpb = std::min(1.0, 1.0 - std::exp(-static_cast<double>(pd.r) / std::ldexp(1.0, kPack2L1Bits)));
+    }
     if (rq.kernel != 0 && !std::isfinite(best.cost)) {
       *err = "the requested scan kernel cannot run this pattern set / option combination";
       return kBadConfig;
@@ -691,12 +731,20 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       sp.ddepth = best.ddepth;
       best_warps = best.warps;
       sp.roll = best.roll;
+      sp.pack2 = best.pack2;
+      sp.pack_shift = best.pack_shift;
       best_halo = best.halo;
       if (best.roll) {
         sp.roll_words = best.roll_words;
         sp.entries = static_cast<uint64_t>(best.roll_words) * 32;
         sp.table_bits = 0;
         sp.blocks = 0;
+      }
+      if (best.pack2) {  // level-1 bitmap of the first 10 symbols' codes
+        sp.table_bits = kPack2L1Bits;
+        sp.entries = 1ull << kPack2L1Bits;
+        sp.blocks = 0;
+        sp.probes = 1;
       }
     }
     sp.pf_bits = best.pf;
@@ -734,6 +782,13 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   if (sp.direct) {  // direct kernel: slices of whole steps, ~32 KiB of text
     const uint64_t step = direct_step_bytes(sp.q) / sp.q;
     P->slice_samples = step * std::max<uint64_t>(1, 32768 / direct_step_bytes(sp.q));
+  }
+  if (sp.pack2) {  // pack2 geometry: 2 KiB steps, 16 steps per slice
+    P->chunk_samples = kPack2Step;
+    P->slice_samples = static_cast<uint64_t>(kPack2Step) * 16;
+    P->back = best_halo;
+    P->ring = kPack2Depth;
+    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
   }
   if (sp.roll) {  // roll kernel geometry: 2 KiB steps, 16 steps per slice
     P->chunk_samples = kRollStep;
@@ -789,6 +844,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
 
 size_t plan_smem(const Plan& p) {
   if (p.sp.direct) return direct_smem(p.sp, p.nwarps);
+  if (p.sp.pack2) return pack2_smem(p.sp.table_bytes, p.back, p.nwarps);
   if (p.sp.roll) return roll_smem(p.sp.roll_words, p.back, p.nwarps);
   return smem_layout(p.sp, p.slot_bytes, p.ring, p.nwarps).total;
 }
@@ -841,6 +897,15 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
   table->assign(sp.table_bytes, 0xff);
   if (sp.verify_all) {
     table->assign(sp.table_bytes, 0);
+    return;
+  }
+  if (sp.pack2) {  // level-1 bitmap: codes of the patterns' first 10 symbols (bit set = present)
+    table->assign(sp.table_bytes, 0);
+    uint32_t* w = reinterpret_cast<uint32_t*>(table->data());
+    for (size_t i = 0; i < pd.r; ++i) {
+      const uint32_t c = pack2_code(pd.pattern(i), kPack2L1Bits / 2, sp.pack_shift);
+      w[c >> 5] |= 1u << (c & 31);
+    }
     return;
   }
   if (sp.roll) {  // Bloom words of the patterns' q-byte prefix hashes (bit set = present)
@@ -922,6 +987,32 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   // inserted in id order, so equal keys are met in id order along a probe run
   pt->vtab.assign(8 * 16, 0);
   pt->vmask = 0;
+  if (sp.pack2) {  // level 2: open addressing by the exact code of the first kb = q symbols
+    size_t slots = 16;
+    uint32_t bits = 4;
+    while (slots < 4 * r) {
+      slots <<= 1;
+      ++bits;
+    }
+    pt->vmask = static_cast<uint32_t>(slots - 1);
+    pt->vbits = bits;
+    pt->vtab.assign(8 * slots, 0);
+    for (size_t i = 0; i < slots; ++i) pt->vtab[8 * i + 1] = 0xffffffffu;
+    for (size_t i = 0; i < r; ++i) {
+      const uint32_t code = pack2_code(pd.pattern(i), sp.q, sp.pack_shift);
+      size_t s = pack2_home(code, bits);
+      while (pt->vtab[8 * s + 1] != 0xffffffffu) s = (s + 1) & pt->vmask;
+      uint32_t* e = &pt->vtab[8 * s];
+      e[0] = code;
+      e[1] = static_cast<uint32_t>(i);
+      e[2] = pd.len[i];
+      e[3] = static_cast<uint32_t>(pd.off[i] / 16);
+      std::memcpy(e + 4, pd.pattern(i), 16);
+    }
+    for (size_t i = 0; i < slots; ++i)
+      if (pt->vtab[8 * i + 1] != 0xffffffffu && pt->vtab[8 * ((i + 1) & pt->vmask) + 1] != 0xffffffffu)
+        pt->vtab[8 * i + 2] |= 0x80000000u;
+  }
   if (sp.roll) {
     size_t slots = 16;
     while (slots < 4 * r) slots <<= 1;  // load factor <= 1/4

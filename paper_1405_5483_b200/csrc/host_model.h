@@ -116,6 +116,7 @@ struct PatternTable {
   // {key, pid (0xffffffff = empty), len, pattern offset / 16, first 16 bytes}
   std::vector<uint32_t> vtab;
   uint32_t vmask = 0;
+  uint32_t vbits = 0;  // pack2: log2 slots
 };
 void build_pattern_table(const Plan& plan, const PatternData& pd, PatternTable* pt);
 

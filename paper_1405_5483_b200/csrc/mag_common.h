@@ -152,6 +152,9 @@ struct ScanPlan {
   uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
+  int pack2;              // dense 2-bit-code scan (<= 4 pattern symbols): every position
+  uint32_t pack_shift;    // pack2: symbol map b -> (b >> pack_shift) & 3
+  uint32_t vbits;         // pack2: log2 level-2 slots
   uint32_t entry_log2;    // log2(bits per mask entry), 0..6
   uint64_t entries;       // number of mask entries
   uint64_t table_bytes;   // packed table size (multiple of 16)
@@ -230,6 +233,24 @@ MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
   return align16(size_t(words) * 4) + size_t(nwarps) * kRollDepth * roll_slot_bytes(halo) +
          size_t(nwarps) * kRollDepth * (32 + 8) + size_t(nwarps) * kRollList * 2 + 64;
 }
+
+// Pack2 kernel: 2^20-bit level-1 bitmap, per-warp ring of kPack2Depth slots
+// of kPack2Step positions + halo, step descriptors, per-warp hit list.
+constexpr int kPack2Step = 2048;
+constexpr int kPack2Depth = 2;
+constexpr int kPack2List = 256;   // listed level-1 hits per round (uint2 {code, position})
+constexpr int kPack2Batch = 2;    // listed hits per lane with level-2 loads in flight
+constexpr uint32_t kPack2L1Bits = 20;  // level-1 key: the first 10 symbols
+MAG_HD size_t pack2_smem(uint64_t table_bytes, uint32_t halo, uint32_t nwarps) {
+  return align16(table_bytes) + size_t(nwarps) * kPack2Depth * align16(kPack2Step + halo) +
+         size_t(nwarps) * kPack2Depth * (32 + 8) + size_t(nwarps) * kPack2List * 8 + 64;
+}
+MAG_HD uint32_t pack2_code(const uint8_t* p, unsigned len, uint32_t shift) {
+  uint32_t c = 0;
+  for (unsigned i = 0; i < len; ++i) c |= ((static_cast<uint32_t>(p[i]) >> shift) & 3u) << (2 * i);
+  return c;
+}
+MAG_HD uint32_t pack2_home(uint32_t code, uint32_t vbits) { return (code * 0x9E3779B1u) >> (32 - vbits); }
 
 MAG_HD SmemLayout smem_layout(const ScanPlan& p, uint32_t slot_bytes, uint32_t ring,
                               uint32_t nwarps) {

@@ -193,6 +193,7 @@ namespace {
 cudaError_t launch_scan_only(const ScanArgs& a, cudaStream_t stream, int grid) {
   if (a.plan.direct) return launch_direct(a, stream, grid);
   if (a.plan.roll) return launch_roll(a, stream, grid);
+  if (a.plan.pack2) return launch_pack2(a, stream, grid);
   if (a.plan.smag) return launch_staged_codes(a, stream, grid);
   if (a.plan.gram_mode == kGramHashed) return launch_staged_hashed(a, stream, grid);
   return launch_staged_exact(a, stream, grid);

@@ -110,6 +110,7 @@ unsigned long long kernel_launch_count();
 // ---- internal: per-family launchers (scan_*.cu)
 cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid);
 cudaError_t launch_roll(const ScanArgs& a, cudaStream_t stream, int grid);
+cudaError_t launch_pack2(const ScanArgs& a, cudaStream_t stream, int grid);
 cudaError_t launch_staged_exact(const ScanArgs& a, cudaStream_t stream, int grid);
 cudaError_t launch_staged_hashed(const ScanArgs& a, cudaStream_t stream, int grid);
 cudaError_t launch_staged_codes(const ScanArgs& a, cudaStream_t stream, int grid);

@@ -510,3 +510,54 @@ def test_text_beyond_2p32_samples(mag, q):
     assert got == sorted(want), (got, sorted(want))
     del prep, d
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("alphabet", [b"ACGT", b"acgt", b"AT", b"xyz"])
+def test_pack2_kernel(mag, ref, alphabet):
+    """The dense 2-bit exact-code scan (forced): texts of every length class
+    around its 2 KiB step and 32 KiB slice, pattern lengths 10..40 (level-2
+    key of min(m, 16) symbols; longer ones finish in global memory),
+    duplicate patterns, dense plants, text bytes outside the pattern alphabet
+    (they collide in the 2-bit map), misaligned device text; the candidate
+    counter equals the restated level-1 filter."""
+    from pyoracle import pack2_candidates
+    rng = np.random.default_rng(90 + len(alphabet))
+    al = np.frombuffer(alphabet, dtype=np.uint8)
+    sizes = [0, 9, 10, 11, 2047, 2048, 2049, 2063, 32768 + 13, 100000, 300001]
+    for it, n in enumerate(sizes):
+        m = int(rng.choice([10, 11, 12, 15, 16, 17, 24, 40]))
+        text = al[rng.integers(0, al.size, n)]
+        if it % 2 and n > 100:  # bytes outside the pattern alphabet
+            text = text.copy()
+            text[rng.integers(0, n, n // 50)] = ord("N")
+        r = int(rng.integers(1, 400))
+        pats = []
+        for _ in range(r):
+            L = m + int(rng.integers(0, 4))
+            if n > L and rng.random() < 0.6:
+                s0 = int(rng.integers(0, n - L + 1))
+                cand = text[s0:s0 + L]
+                if np.isin(cand, al).all():
+                    pats.append(cand.tobytes())
+                    continue
+            pats.append(al[rng.integers(0, al.size, L)].tobytes())
+        pats.append(pats[0])  # duplicate pattern id
+        text = text.copy()
+        for _ in range(n // 40):
+            p = pats[int(rng.integers(0, len(pats)))]
+            if len(p) < n:
+                s0 = int(rng.integers(0, n - len(p) + 1))
+                text[s0:s0 + len(p)] = np.frombuffer(p, dtype=np.uint8)
+        e = mag.Engine(pats, scan_kernel="pack2")
+        pl = e.plan()
+        assert pl["pack2"] == 1, pl
+        got, met = gpu_pairs(e, text)
+        assert got == as_pairs(*ref.ac(text, pats)), (n, m, pl)
+        shift = next(s for s in range(7) if len({(c >> s) & 3 for c in set(b"".join(pats))}) == len(set(b"".join(pats))))
+        assert met.filter_reads == max(0, n - pl["q"] + 1)
+        assert met.candidates == pack2_candidates(text, pats, pl["q"], shift), (n, m)
+        if n > 64:
+            import torch
+            d = torch.from_numpy(text).cuda()
+            pd = e.prepare_device(d.data_ptr() + 5, n - 5, keep=d)
+            assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[5:], pats))
