@@ -120,8 +120,8 @@ struct Pack2Scanner {
 #pragma unroll
     for (int p = 0; p < kRun; ++p) {
       const uint32_t lo = p < 16 ? pk[0] : pk[1], hi = p < 16 ? pk[1] : pk[2];
-      const uint32_t code = __funnelshift_r(lo, hi, 2 * p);       // bit test: code & 31
-      const uint32_t w5 = __funnelshift_r(lo, hi, 2 * p + 5);     // word: (code >> 5) & 0x7fff
+      const uint32_t code = __funnelshift_r(lo, hi, 2 * p);  // symbols p .. p + 15; bit test: code & 31
+      const uint32_t w5 = code >> 5;                            // word: (code >> 5) & 0x7fff
       uint32_t addr, wd;
       asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(w5 & 0x7fffu), "r"(tbl_s));
       asm("ld.shared.u32 %0, [%1];" : "=r"(wd) : "r"(addr));
