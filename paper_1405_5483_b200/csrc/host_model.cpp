@@ -988,9 +988,9 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   pt->vtab.assign(8 * 16, 0);
   pt->vmask = 0;
   if (sp.pack2) {  // level 2: open addressing by the exact code of the first kb = q symbols
-    size_t slots = 16;
+    size_t slots = 16;  // load factor <= 1/8: a missing key's home slot is empty 7 times in 8
     uint32_t bits = 4;
-    while (slots < 4 * r) {
+    while (slots < 8 * r) {
       slots <<= 1;
       ++bits;
     }

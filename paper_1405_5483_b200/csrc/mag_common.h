@@ -239,7 +239,7 @@ MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
 constexpr int kPack2Step = 2048;
 constexpr int kPack2Depth = 2;
 constexpr int kPack2List = 256;   // listed level-1 hits per round (uint2 {code, position})
-constexpr int kPack2Batch = 2;    // listed hits per lane with level-2 loads in flight
+constexpr int kPack2Batch = 6;    // listed hits per lane with level-2 loads in flight
 constexpr uint32_t kPack2L1Bits = 20;  // level-1 key: the first 10 symbols
 MAG_HD size_t pack2_smem(uint64_t table_bytes, uint32_t halo, uint32_t nwarps) {
   return align16(table_bytes) + size_t(nwarps) * kPack2Depth * align16(kPack2Step + halo) +

@@ -179,34 +179,41 @@ struct Pack2Scanner {
     return c;
   }
 
-  // Level 2 + output of the listed hits [0, total) in text order, up to
-  // kPack2Batch per lane with all their slot loads in flight together.
+  // Level 2 + output of the listed hits [0, total) in text order,
+  // kPack2Batch per lane at a time: the key halves of their home slots load
+  // together (one round trip per batch), then the pattern-byte halves of the
+  // code hits only, then the compares against the staged text.
   __device__ void verify_list(const uint32_t* sw, unsigned long long t, uint32_t total) {
-    const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0);
-    for (uint32_t base = 0; base < total; base += 32 * kPack2Batch) {
-      uint32_t code[kPack2Batch], pr[kPack2Batch];
-      uint4 hq[kPack2Batch], bq[kPack2Batch];
+    constexpr int kB = kPack2Batch;
+    const uint4 empty = make_uint4(0, 0xffffffffu, 0, 0), zero = make_uint4(0, 0, 0, 0);
+    for (uint32_t base = 0; base < total; base += 32 * kB) {
+      uint32_t code[kB], pr[kB];
+      uint4 hq[kB], bq[kB];
+      bool hit[kB], more[kB];
 #pragma unroll
-      for (int k = 0; k < kPack2Batch; ++k) {
+      for (int k = 0; k < kB; ++k) {
         const uint32_t rank = base + 32 * k + lane;
         const bool live = rank < total;
         const uint2 e = live ? list[rank] : make_uint2(0u, 0u);
         code[k] = e.x & kmask;
         pr[k] = e.y;
-        const uint32_t s = home(code[k]);
-        hq[k] = live ? __ldg(A.vtab + 2 * s) : empty;
-        bq[k] = live ? __ldg(A.vtab + 2 * s + 1) : empty;
+        hq[k] = live ? __ldg(A.vtab + 2 * home(code[k])) : empty;
       }
 #pragma unroll
-      for (int k = 0; k < kPack2Batch; ++k) {
-        // the code decides almost every candidate: text bytes only for a code hit
-        const bool code_hit = hq[k].y != 0xffffffffu && hq[k].x == code[k];
-        const bool more = hq[k].y != 0xffffffffu && (hq[k].z >> 31);
-        uint4 tx = make_uint4(0, 0, 0, 0);
-        if (__any_sync(kFull, code_hit || more)) tx = text16(sw, pr[k]);
-        uint32_t c = code_hit && slot_match(t + pr[k], tx, code[k], hq[k], bq[k]) ? 1u : 0u;
-        uint32_t pid0 = hq[k].y;
-        if (__any_sync(kFull, more) && more) c = probe_rest(t + pr[k], tx, code[k], nullptr, 0, c, &pid0);
+      for (int k = 0; k < kB; ++k) {
+        hit[k] = hq[k].y != 0xffffffffu && hq[k].x == code[k];
+        more[k] = hq[k].y != 0xffffffffu && (hq[k].z >> 31);
+        bq[k] = hit[k] ? __ldg(A.vtab + 2 * home(code[k]) + 1) : zero;
+      }
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        uint32_t c = 0, pid0 = hq[k].y;
+        uint4 tx = zero;
+        if (__any_sync(kFull, hit[k] || more[k])) {
+          tx = text16(sw, pr[k]);
+          c = hit[k] && slot_match(t + pr[k], tx, code[k], hq[k], bq[k]) ? 1u : 0u;
+          if (__any_sync(kFull, more[k]) && more[k]) c = probe_rest(t + pr[k], tx, code[k], nullptr, 0, c, &pid0);
+        }
         const unsigned one = __ballot_sync(kFull, c == 1u);
         if (!__any_sync(kFull, c > 1u)) {  // one pattern per start (the common case)
           if (c) {
@@ -223,36 +230,14 @@ struct Pack2Scanner {
           if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], pid0);
         } else if (c > 1) {
           uint32_t w = 0;
-          if (code_hit && slot_match(t + pr[k], tx, code[k], hq[k], bq[k])) {
+          if (hit[k] && slot_match(t + pr[k], tx, code[k], hq[k], bq[k])) {
             if (fill + ex < A.slice_cap) out[fill + ex] = pack_match(t + pr[k], hq[k].y);
             w = 1;
           }
-          if (more) probe_rest(t + pr[k], tx, code[k], out, fill + ex, w, nullptr);
+          if (more[k]) probe_rest(t + pr[k], tx, code[k], out, fill + ex, w, nullptr);
         }
         fill += tc;
       }
-    }
-  }
-
-  // List the level-1 hits of one run set (masks h of all lanes, run offset
-  // roff) in text order, kPack2List at a time, and verify them.
-  __device__ __forceinline__ void list_and_verify(const uint32_t* sw, unsigned long long t, uint32_t h,
-                                                  const uint32_t (&pk)[3], uint32_t roff) {
-    const uint32_t c = __popc(h);
-    const uint32_t e = warp_excl_scan(c, lane);
-    const uint32_t total = __shfl_sync(kFull, e + c, 31);
-    cands32 += c;
-    if (A.plan.diag & 8) return;
-    for (uint32_t r0 = 0; r0 < total; r0 += kPack2List) {
-      uint32_t idx = e;
-      for (uint32_t m = h; m; m &= m - 1, ++idx) {
-        if (idx < r0 || idx >= r0 + kPack2List) continue;
-        const int p = __ffs(m) - 1;
-        list[idx - r0] = make_uint2(code_at(pk, p), roff + 32u * lane + static_cast<uint32_t>(p));
-      }
-      __syncwarp();
-      verify_list(sw, t, min(total - r0, static_cast<uint32_t>(kPack2List)));
-      __syncwarp();
     }
   }
 
@@ -273,15 +258,40 @@ struct Pack2Scanner {
       }
       const uint8_t* sb = slots + static_cast<size_t>(j) * slot_bytes;
       const uint32_t* sw = reinterpret_cast<const uint32_t*>(sb);
-#pragma unroll 1
-      for (int r = 0; r < 2; ++r) {
-        const int b = 1024 * r + 32 * lane;
-        uint32_t pk[3];
-        uint32_t h = filter_run(sb, b, pk);
-        // positions past the step's valid range never hit
+      // both runs' level 1 (run r: positions [1024 r + 32 lane, + 32))
+      uint32_t pk0[3], pk1[3];
+      uint32_t h0 = filter_run(sb, 32 * lane, pk0);
+      uint32_t h1 = filter_run(sb, 1024 + 32 * lane, pk1);
+      auto keep = [&](int b) -> uint32_t {  // positions past the step's valid range never hit
         const int left = static_cast<int>(lim) - b;
-        h &= left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
-        list_and_verify(sw, d.t, h, pk, 1024u * r);
+        return left >= 32 ? 0xffffffffu : (left <= 0 ? 0u : ((1u << left) - 1u));
+      };
+      h0 &= keep(32 * lane);
+      h1 &= keep(1024 + 32 * lane);
+      // one list per step in text order: run 0's hits, then run 1's
+      const uint32_t c0 = __popc(h0), c1 = __popc(h1);
+      const uint32_t packed = warp_excl_scan(c0 | (c1 << 16), lane);
+      const uint32_t tot = __shfl_sync(kFull, packed + (c0 | (c1 << 16)), 31);
+      const uint32_t t0 = tot & 0xffffu, total = t0 + (tot >> 16);
+      cands32 += c0 + c1;
+      if (!(A.plan.diag & 8)) {
+        for (uint32_t r0 = 0; r0 < total; r0 += kPack2List) {
+          uint32_t idx = packed & 0xffffu;
+          for (uint32_t m = h0; m; m &= m - 1, ++idx)
+            if (idx >= r0 && idx < r0 + kPack2List) {
+              const int p = __ffs(m) - 1;
+              list[idx - r0] = make_uint2(code_at(pk0, p), 32u * lane + static_cast<uint32_t>(p));
+            }
+          idx = t0 + (packed >> 16);
+          for (uint32_t m = h1; m; m &= m - 1, ++idx)
+            if (idx >= r0 && idx < r0 + kPack2List) {
+              const int p = __ffs(m) - 1;
+              list[idx - r0] = make_uint2(code_at(pk1, p), 1024u + 32u * lane + static_cast<uint32_t>(p));
+            }
+          __syncwarp();
+          verify_list(sw, d.t, min(total - r0, static_cast<uint32_t>(kPack2List)));
+          __syncwarp();
+        }
       }
       if (flags & 2u) publish_slice(A, d.slice, fill, lane);
       __syncwarp();
