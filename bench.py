@@ -129,9 +129,29 @@ class ClockSampler:
                 "samples": len(self.samples), "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def cpu_reference(workload, budget_s=12.0, threads=None):
-    """Reference Aho–Corasick (oracle/_ref) over a bounded sample of the text,
-    chunk-parallel on `threads` host cores.  Returns (GB/s, cores, sample)."""
+def plan_kernel(plan):
+    for k in ("direct", "roll", "pack2"):
+        if plan.get(k):
+            return k
+    return "scan"
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference(workload, threads=None):
+    """Reference Aho–Corasick (oracles.cpp:78-95, compiled unmodified into
+    oracle/_ref) over the WHOLE text of the workload (the same config as the
+    GPU arm), chunk-parallel on `threads` host cores with maxlen-1 bytes of
+    look-ahead per chunk.  Returns (GB/s, cores, sample, kind)."""
     from pyoracle import REF_SO, Port, Ref
     threads = threads or os.cpu_count() or 1
     text, pats = workload.text, workload.patterns
@@ -142,23 +162,71 @@ def cpu_reference(workload, budget_s=12.0, threads=None):
         port, kind = Port(), "port"
         run = lambda t: port.naive(t, pats)
         threads = 1
-    probe = min(text.size, 1 << 20)
+        text = text[: 1 << 24]
     t0 = time.perf_counter()
-    run(text[:probe])
-    dt = max(time.perf_counter() - t0, 1e-6)
-    rate = probe / dt  # bytes/s incl. automaton build
-    size = int(min(text.size, max(probe, rate * budget_s)))
-    t0 = time.perf_counter()
-    run(text[:size])
+    run(text)
     dt = time.perf_counter() - t0
-    sample = f"first {size} bytes of the {workload.name} text, {threads} threads, AC build included"
-    return size / dt / 1e9, threads, sample, kind
+    sample = (f"whole {workload.name} text ({text.size} bytes), {threads} threads, automaton build included, "
+              f"host CPU {cpu_model()}")
+    return text.size / dt / 1e9, threads, sample, kind
 
 
-def config_sweep(cfgs, local, steps=10, warmup=3):
-    """Every other BASELINE.json config, device-resident: step and scan-kernel
-    GB/s, fraction of HBM, the plan, and whether the full-size match set's
-    count + sha256 equal the reference AC's (tests/golden/full_digests.json)."""
+def mag_restated_baseline(workload, threads, cap_s=8.0):
+    """The restated reference MAG engine (oracle/mag_oracle.c mo_search:
+    engine.hpp:79-85 -> filter.hpp:51-74 -> brute-force verify_window
+    verify.hpp:28-31) at REFERENCE-DEFAULT parameters: the balanced map over
+    the pattern histogram (mag.h:47, alphabet_map.cpp:90-102), the restated
+    tuner's q and k (tuner.hpp:38-66).  Timed on doubling text prefixes until
+    a run takes cap_s/4 or the whole text ran; threads > 1 split the prefix
+    into chunks with maxlen-1 look-ahead (the chunk contract).
+    Returns a dict; `extrapolated` when the prefix is shorter than the text."""
+    from concurrent.futures import ThreadPoolExecutor
+    import numpy as np
+    from pyoracle import Port
+    port = Port()
+    text, pats = workload.text, workload.patterns
+    allb = np.frombuffer(b"".join(pats), dtype=np.uint8)
+    counts = np.bincount(allb, minlength=256).astype(np.uint64)
+    sigma = int((counts > 0).sum())
+    sp = sigma if sigma <= 64 else 256
+    table, sp = port.map_build(2 if sp < 256 else 0, counts, max(sp, 2))
+    m = min(len(p) for p in pats)
+    tu = port.tune(sigma, len(pats), m, n=text.size)
+    P = port.params(variant=0, gram_mode=0, q=tu["q"], k=tu["k"], sigma_prime=sp, table=table)
+    look = max(len(p) for p in pats) - 1
+
+    def run(size):
+        if threads <= 1:
+            port.search(text[:size], pats, P)
+            return
+        bounds = [size * c // threads for c in range(threads + 1)]
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(lambda c: port.search(text[bounds[c]:min(size, bounds[c + 1] + look)], pats, P),
+                        range(threads)))
+
+    size, dt = 1 << 12, 0.0
+    while True:
+        t0 = time.perf_counter()
+        run(size)
+        dt = time.perf_counter() - t0
+        if dt >= cap_s / 4 or size >= text.size:
+            break
+        size = min(text.size, size * 4 if dt < cap_s / 64 else size * 2)
+    gbs = size / dt / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+            "params": {"q": tu["q"], "k": tu["k"], "sigma_prime": sp, "mapping": "balance" if sp < 256 else "identity"},
+            "sample": f"first {size} bytes of the {workload.name} text ({dt:.2f} s)",
+            "extrapolated": size < text.size,
+            "note": "prefix-extrapolated to the whole text" if size < text.size else "whole text"}
+
+
+def config_sweep(cells, local, steps=10, warmup=3):
+    """BASELINE.json configs, device-resident: step and scan GB/s, fraction of
+    HBM, the plan, and whether the full-size match set's count + sha256 equal
+    the reference AC's (tests/golden/full_digests.json).  `cells` holds
+    (config, label, engine kwargs): the planner's plan ({}) and the
+    reference-default exact-code plan (gram_mode=0: the restated tuner's q/k,
+    the balanced map, m' = min(L/k, w/k) -- tuner.hpp:38-66, filter.hpp:51-74)."""
     import hashlib
     import numpy as np
     import torch
@@ -168,9 +236,14 @@ def config_sweep(cfgs, local, steps=10, warmup=3):
     with open(os.path.join(ROOT, "tests", "golden", "full_digests.json")) as f:
         digests = json.load(f)
     out = {}
-    for c in cfgs:
-        w = workloads.generate(c, 1.0)
-        eng = mag.Engine(w.patterns, device=local)
+    cache = {}
+    for c, label, kw in cells:
+        if c not in cache:
+            cache.clear()
+            torch.cuda.empty_cache()
+            cache[c] = workloads.generate(c, 1.0)
+        w = cache[c]
+        eng = mag.Engine(w.patterns, device=local, **kw)
         d = torch.from_numpy(w.text).to(f"cuda:{local}")
         prep = eng.prepare_device(d.data_ptr(), w.text.size, keep=d)
         m = eng.search_prepared(prep)
@@ -180,34 +253,42 @@ def config_sweep(cfgs, local, steps=10, warmup=3):
         h.update(np.ascontiguousarray(pids, dtype="<u4").tobytes())
         want = digests.get(str(c), {})
         ok = int(offs.size) == want.get("matches") and h.hexdigest() == want.get("matches_sha256")
+        met = m.metrics()
         m.close()
         st = torch.cuda.Stream()
         for _ in range(warmup):
             eng.search_prepared_async(prep, st.cuda_stream).close()
-        # inputs below L2 size (cfg1, 16 MiB) are re-read from L2: flush it
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}") if w.text.size < (256 << 20) else None
+        # inputs below L2 size (cfg1, 16 MiB): a read-only pass over 256 MiB
+        # between steps evicts them without leaving dirty lines to write back
+        flush = (torch.ones(64 << 20, dtype=torch.int32, device=f"cuda:{local}")
+                 if w.text.size < (256 << 20) else None)
         torch.cuda.synchronize()
         mag.scan_timer(True)
         ms = 0.0
-        for _ in range(steps):
-            if flush is not None:
-                flush.fill_(1)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            eng.search_prepared_async(prep, st.cuda_stream).close()
-            e1.record(st)
-            torch.cuda.synchronize()
-            ms += e0.elapsed_time(e1)
+        with torch.cuda.stream(st):
+            for _ in range(steps):
+                if flush is not None:
+                    flush.sum()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                eng.search_prepared_async(prep, st.cuda_stream).close()
+                e1.record(st)
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
         kms, kl = mag.scan_timer_read()
         mag.scan_timer(False)
         n = int(w.text.size)
         step_gbs = n / (ms / steps * 1e-3) / 1e9
         kern_gbs = n / (kms / max(kl, 1) * 1e-3) / 1e9
         pl = eng.plan()
-        out[f"cfg{c}"] = {"workload": w.name, "n": n, "r": len(w.patterns), "GB/s": step_gbs, "kernel_GB/s": kern_gbs,
-                          "frac_of_hbm": kern_gbs / peak, "matches": int(offs.size), "bit_exact_vs_reference": bool(ok),
-                          "l2": "flushed between steps" if flush is not None else "input larger than L2",
-                          "plan": {k: pl[k] for k in ("variant", "q", "k", "m_prime", "probes", "direct", "roll")}}
+        out[f"cfg{c}{label}"] = {
+            "workload": w.name, "n": n, "r": len(w.patterns), "GB/s": step_gbs, "kernel_GB/s": kern_gbs,
+            "frac_of_hbm": kern_gbs / peak, "step_frac_of_hbm": step_gbs / peak, "matches": int(offs.size),
+            "filter_reads": met.filter_reads, "candidates": met.candidates, "bit_exact_vs_reference": bool(ok),
+            "l2": "read-only 256 MiB pass between steps" if flush is not None else "input larger than L2",
+            "plan": {k: pl[k] for k in ("variant", "gram_mode", "q", "k", "m_prime", "sigma_prime", "table_bits",
+                                        "probes", "direct", "roll", "pack2")},
+            "params": "reference-default exact codes (restated tuner, balanced map)" if kw else "GPU planner"}
         del d, prep, eng, flush
         torch.cuda.empty_cache()
     return out
@@ -236,20 +317,21 @@ def main():
         w = workloads.generate(args.config, args.scale)
         vals = []
         for _ in range(max(args.warmup, 0)):
-            cpu_reference(w, budget_s=1.0)
+            cpu_reference(w)
         info = None
         for _ in range(max(args.steps, 1)):
-            gbs, cores, sample, kind = cpu_reference(w, budget_s=4.0)
+            gbs, cores, sample, kind = cpu_reference(w)
             vals.append(gbs)
             info = (cores, sample, kind)
         v = sorted(vals)[len(vals) // 2]
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": w.text.size / (v * 1e9) * 1e3,
+                "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
                 "config": {"workload": w.name, "n": int(w.text.size), "r": len(w.patterns),
                            "m": w.meta["m"], "parallelism": "cpu threads"},
                 "cpu_baseline": {"value": v, "unit": "GB/s", "cores": info[0], "kind": info[2],
-                                 "sample": info[1]},
+                                 "sample": info[1], "cpu_model": cpu_model(), "same_config": True},
                 "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -347,7 +429,7 @@ def main():
         offs, pids = shard.clip(offs, pids, 0, n)
         got = shard.gather(offs + np.uint64(rank * n), pids, world, rank)
         e2e_t.append(time.perf_counter() - t0)
-        d2h = len(m) * 12 + 32
+        d2h = len(m) * 8 + 4 * 8  # sorted 8-byte match keys + the mapped counter words
         if got is not None:
             total_matches = int(got[0].size)
         m.close()
@@ -365,21 +447,30 @@ def main():
     peak, peak_src = peaks()
     kernel_ms = kernel_ms_total / max(kernel_launches, 1)
     achieved = n / (kernel_ms * 1e-3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
             with open(tp) as f:
-                traffic = json.load(f).get(f"cfg{args.config}")
+                tj = json.load(f)
+            traffic = tj.get(f"cfg{args.config}")
+            traffic_src = "static, not measured in this run: " + tj.get("source", "")
         except Exception:
             traffic = None
     sweep = None
     if not args.headline_only and world == 1:
-        sweep = config_sweep([c for c in (1, 2, 3, 4, 5) if c != args.config], local)
+        cells = []
+        for c in (1, 2, 3, 4, 5):
+            if c != args.config:
+                cells.append((c, "", {}))
+            cells.append((c, "_reference_params", {"gram_mode": 0}))
+        sweep = config_sweep(cells, local)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         gbs, cores, sample, kind = cpu_reference(w)
-        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample}
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": kind, "sample": sample,
+               "cpu_model": cpu_model(), "same_config": args.scale == 1.0,
+               "mag_restated": [mag_restated_baseline(w, 1), mag_restated_baseline(w, os.cpu_count() or 1)]}
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
@@ -395,8 +486,10 @@ def main():
                    "candidates": metrics.candidates, "checked_vs_reference_ac": checked,
                    "bit_exact_vs_reference_digest": digest_ok},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": n},
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_source": peak_src, "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": n,
+                     "kernel": f"mag_{plan_kernel(plan)}_kernel + mag_finish_kernel (one search = these two "
+                               "launches; CUDA events around them on the launch stream)"},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(span.size), "d2h_bytes_per_step": d2h,
                 "api": "mag_search (pinned host text) + clip + rank-ordered gather"},

@@ -104,3 +104,52 @@ def test_search_tsv(cli, tmp_path, ref):
     assert out.returncode == 0 and out.stdout == want
     out = run(cli, "search", "--patterns", str(p), "--text", str(t), "--count")
     assert out.stdout == f"{offs.size}\n"
+
+
+BENCH_HEADER = ("dataset,variant,r,m,q,k,sigma_prime,mapping,mb_per_s,filter_reads,candidates,"
+                "occurrences")  # BenchRow field list, in order
+
+
+def test_bench_header_and_usage(cli, tmp_path):
+    assert run(cli, "bench").returncode == 2
+    assert run(cli, "bench", "--text", "/nonexistent").returncode == 2
+    t = tmp_path / "t.txt"
+    t.write_bytes(b"ACGT" * 100)
+    assert run(cli, "bench", "--text", str(t), "--r", "x").returncode == 2
+    assert run(cli, "bench", "--text", str(t), "--variant", "mag,bogus").returncode == 2
+    out = run(cli, "bench", "--text", str(t), "--r", "2", "--m", "8")
+    assert out.stdout.split("\n")[0] == BENCH_HEADER
+    import torch
+    if not torch.cuda.is_available():
+        assert out.returncode == 1 and "CUDA" in out.stderr
+
+
+@pytest.mark.gpu
+def test_bench_matrix(cli, tmp_path, ref):
+    """2 variants x 2 r x 1 m -> 4 rows; --check passes and every
+    occurrences column equals the reference AC count for the same sample."""
+    import paper_1405_5483_b200 as mag
+    rng = np.random.default_rng(11)
+    text = np.frombuffer(b"ACGT", np.uint8)[rng.integers(0, 4, 1 << 20)]
+    t = tmp_path / "dna.txt"
+    t.write_bytes(text.tobytes())
+    out = run(cli, "bench", "--text", str(t), "--name", "dna1m", "--variant", "mag,shiftor_og",
+              "--r", "10,1000", "--m", "16", "--seed", "5", "--reps", "2", "--check")
+    assert out.returncode == 0, out.stderr
+    lines = out.stdout.strip().split("\n")
+    assert lines[0] == BENCH_HEADER and len(lines) == 5
+    for row in lines[1:]:
+        f = row.split(",")
+        assert f[0] == "dna1m" and f[1] in ("mag", "shiftor_og") and f[3] == "16"
+        r = int(f[2])
+        pats = mag.sample_patterns(text, r, 16, 5)
+        offs, _ = ref.ac(text, pats)
+        assert int(f[11]) == offs.size >= r  # every sampled pattern occurs at its source
+        assert float(f[8]) > 0 and int(f[9]) > 0
+    # --include-prep and reference-mode parameters: q/k/sigma'/mapping echoed
+    out = run(cli, "bench", "--text", str(t), "--r", "100", "--m", "32", "--include-prep", "--check",
+              "--q", "4", "--k", "1", "--sigma-prime", "4", "--mapping", "balance", "--reps", "1",
+              "--variant", "smag")
+    assert out.returncode == 0, out.stderr
+    f = out.stdout.strip().split("\n")[1].split(",")
+    assert f[1] == "smag" and f[4:8] == ["4", "1", "4", "balance"]

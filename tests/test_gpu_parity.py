@@ -125,6 +125,7 @@ def test_hashed_counters_match_port(mag, ref, port):
             assert met.filter_reads == max(0, text.size - pl["q"] + 1)
             assert met.candidates == roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, pl["probes"])
             continue
+        assert not pl["pack2"], pl  # never planned automatically
         P = port.params(variant=0 if pl["variant"] == 0 else 2, gram_mode=1, q=pl["q"], k=pl["k"],
                         table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
                         blocks=pl["blocks"])
@@ -308,6 +309,31 @@ def test_full_configs(mag, cfg):
     offs, pids = m.arrays()
     assert offs.size == want["matches"], (cfg, e.plan())
     assert match_digest(offs, pids) == want["matches_sha256"], (cfg, e.plan())
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_configs_reference_params(mag, port, cfg):
+    """The same full-size digests through the reference-default exact-code
+    plan: the restated tuner's q/k (tuner.hpp:38-66), the balanced map over
+    the pattern histogram (alphabet_map.cpp:90-102), m' = min(L/k, w/k)
+    (filter.hpp:27-31) -- the staged Shift-Or kernel with m' = 3 (cfg2), 2
+    (cfg3), 7 (cfg4).  The plan's q/k equal mag_tune's."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_full_digests import match_digest
+    from paper_1405_5483_b200 import workloads
+    want = _full_digests()[str(cfg)]
+    w = workloads.generate(cfg, 1.0)
+    e = mag.Engine(w.patterns, gram_mode=mag.GRAM_EXACT)
+    pl, info = e.plan(), e.info()
+    sigma = len(set(b"".join(w.patterns)))
+    tu = port.tune(sigma, len(w.patterns), w.meta["m"])
+    assert (pl["gram_mode"], info.q, info.k, info.mapping) == (0, tu["q"], tu["k"], mag.MAPPING_BALANCED)
+    assert pl["m_prime"] == min((w.meta["m"] - info.q + 1) // info.q // info.k, 64 // info.k)
+    offs, pids = e.search(w.text).arrays()
+    assert offs.size == want["matches"], (cfg, pl)
+    assert match_digest(offs, pids) == want["matches_sha256"], (cfg, pl)
 
 
 @pytest.mark.parametrize("H", [2, 3])
