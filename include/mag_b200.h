@@ -76,6 +76,15 @@ typedef struct mag_plan_info {
   int roll;             /* dense rolling-hash scan (every position, q-byte prefix Bloom) */
   int cluster;          /* always 0 (kept for ABI stability) */
   int pack2;            /* dense 2-bit exact-code scan (sigma' = 4 codes, two levels) */
+  /* Measured selectivity (mag_options.histogram_sample given, >= 4 KiB): the
+   * plan's own filter, with its real tables, run over up to 1 MiB of that
+   * sample at engine creation.  Replaces the uniform-text estimate of the
+   * reference's cost model (tuner.hpp:58-66) when plans are compared. */
+  double measured_candidates_per_byte; /* -1: no sample was given */
+  uint64_t measured_sample_bytes;
+  double predicted_cost;  /* planner cost, thread-instructions per text byte (analytic rate) */
+  double measured_cost;   /* the same cost re-priced with the measured rate */
+  uint32_t measured_plans; /* finalist plans (one per kernel family) measured on the sample */
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);

@@ -90,7 +90,9 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("warps", C.c_uint32), ("stages", C.c_uint32), ("smem_bytes", C.c_size_t),
         ("predicted_candidates_per_byte", C.c_double), ("probes", C.c_uint32),
         ("blocks", C.c_uint32), ("direct", C.c_int), ("roll", C.c_int), ("cluster", C.c_int),
-        ("pack2", C.c_int),
+        ("pack2", C.c_int), ("measured_candidates_per_byte", C.c_double),
+        ("measured_sample_bytes", C.c_uint64), ("predicted_cost", C.c_double),
+        ("measured_cost", C.c_double), ("measured_plans", C.c_uint32),
     ]
 
 

@@ -636,7 +636,9 @@ MAG_API mag_status mag_engine_create_ex(const uint8_t* const* patterns, const si
     if (opts.base.mapping < -1 || opts.base.mapping > 3)
       return fail(MAG_ERR_BAD_CONFIG, "unknown mapping " + std::to_string(opts.base.mapping));
     std::string err;
-    int ps = make_plan(e->pd, e->hist, rq, &e->plan, &err);
+    // a text sample also prices the finalist plans by their measured candidate rates
+    int ps = make_plan_measured(e->pd, e->hist, rq, opts.base.histogram_sample,
+                                opts.base.histogram_sample ? opts.base.histogram_sample_len : 0, &e->plan, &err);
     if (ps != 0) return fail(static_cast<mag_status>(ps), err);
     build_masks(e->plan, e->pd, &e->table);
     build_pattern_table(e->plan, e->pd, &e->ptab);
@@ -723,6 +725,11 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->roll = P.sp.roll;
   out->cluster = 0;
   out->pack2 = P.sp.pack2;
+  out->measured_candidates_per_byte = P.meas_cand_per_byte;
+  out->measured_sample_bytes = P.meas_sample_bytes;
+  out->predicted_cost = P.pred_cost;
+  out->measured_cost = P.meas_cand_per_byte < 0 ? P.pred_cost : P.meas_cost;
+  out->measured_plans = P.meas_plans;
   return MAG_OK;
 }
 

@@ -305,7 +305,7 @@ void finish_geometry(const PatternData& pd, const PlanRequest& rq, Plan* P) {
       align16(chunk_bytes + static_cast<uint64_t>(ov) * bps + qm1 + extra + P->back + 15));
   P->slot_bytes = P->full_bytes + 32;
   P->ring = rq.stages > 0 ? static_cast<uint32_t>(rq.stages) : kDefaultRing;
-  P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kDefaultWarps;
+  P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kDefaultWarps;
 }
 
 size_t fixed_smem(const Plan& P) {
@@ -448,6 +448,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       bool va = true;
       int og = 0;
       double cpb = 1;
+      double slope = 0;  // d cost / d (candidates per byte): what a measured rate re-prices
+      double surv_slope = 0;  // direct: d cost / d (screen survivors per byte)
     } best;
     best.og = sp.overlapping;
     auto pf_bytes = [](unsigned pf) { return pf ? align16((size_t(1) << pf) / 8) : size_t(16); };
@@ -467,6 +469,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.pf = pf;
           best.chunk = chunk;
           best.cpb = 1;
+          best.slope = 0;
         }
         break;  // largest chunk that fits
       }
@@ -524,11 +527,14 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                 if (!chunk) continue;
                 const double fp = pf ? prefilter_fp(nkeys, pf) : 1.0;
                 double cost = sample_cost + (H - 1) * kCostProbeBit / (og ? 1.0 : static_cast<double>(k * q)) + kCostChunk / chunk;
-                if (wkey)  // window keys: one batched key + L2 screen per candidate
-                  cost += cpb * (kCostCand + kCostWindow + (pf ? kCostPf : 0.0) +
-                                 fp * (kCostScreen + 0.01 * kCostProbe) + hits * kCostCompare);
-                else       // start keys: one probe per verified start
-                  cost += cpb * kCostCand + pm * (kCostStart + fp * kCostProbe + hits * kCostCompare);
+                // per candidate: window keys pay one batched key + L2 screen,
+                // start keys one probe per verified start (q starts per strided candidate)
+                const double per_cand =
+                    wkey ? kCostCand + kCostWindow + (pf ? kCostPf : 0.0) +
+                               fp * (kCostScreen + 0.01 * kCostProbe) + hits * kCostCompare
+                         : kCostCand + (og ? 1.0 : static_cast<double>(q)) *
+                                           (kCostStart + fp * kCostProbe + hits * kCostCompare);
+                cost += cpb * per_cand;
                 cost = staged_scale(cost);
                 if (cost < best.cost * 0.999) {
                   best.cost = cost;
@@ -542,6 +548,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
                   best.va = false;
                   best.og = og;
                   best.cpb = cpb;
+                  best.slope = kStagedScale * per_cand;
                 }
               }
              }
@@ -563,7 +570,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       // measured W = 16 at 13/14/15/16 warps: cfg4 2,551/2,604/2,686/1,934
       // GB/s (a 16th scanning warp leaves L1 ~17 KB for the screen and bucket
       // loads), cfg2 15 vs 16 = 4,802 vs 4,689 GB/s.
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)
@@ -599,8 +606,9 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         const double cpb = p / q;
         // a filter hit only issues its L2 screen load (resolved a step later);
         // ~1/128 of them, plus the true starts, reach a bucket walk
-        const double cost = kStagedScale * (kCostSample + 2 * H * kCostProbeBit) / q +
-                            cpb * (kCostDirectHit + 0.008 * (kCostCand + kCostProbe + hits * kCostCompare));
+        const double per_surv = kCostCand + kCostProbe + hits * kCostCompare;
+        const double per_cand = kCostDirectHit + 0.008 * per_surv;
+        const double cost = kStagedScale * (kCostSample + 2 * H * kCostProbeBit) / q + cpb * per_cand;
         if (cost < best.cost * 0.999) {
           best.cost = cost;
           best.q = q;
@@ -612,6 +620,8 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.chunk = kChunkTarget;
           best.va = false;
           best.cpb = cpb;
+          best.slope = kCostDirectHit;
+          best.surv_slope = per_surv;
           best.direct = 1;
           best.og = 0;
           best.blocks = H > 1 ? blocks : 0;
@@ -632,7 +642,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           q = c;
           break;
         }
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
       const uint32_t v4 = (32 + q - 1 + 15) / 16;
       const uint32_t halo = static_cast<uint32_t>(
           align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
@@ -662,6 +672,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.va = false;
           best.og = 1;
           best.cpb = cpb;
+          best.slope = kCostRollCand;
           best.roll = 1;
           best.roll_words = words;
           best.halo = halo;
@@ -750,6 +761,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.pf_bits = best.pf;
     P->chunk_target = best.chunk;
     P->pred_cand_per_byte = best.cpb;
+    P->pred_cost = best.cost;
+    P->cost_slope = best.slope;
+    P->surv_slope = best.surv_slope;
+    P->pred_surv_per_byte = best.direct ? 0.008 * best.cpb : 0.0;
   }
 
   // ---- machine shape (filter.hpp:27-31, superimpose.cpp:11-21)
@@ -788,14 +803,14 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->slice_samples = static_cast<uint64_t>(kPack2Step) * 16;
     P->back = best_halo;
     P->ring = kPack2Depth;
-    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
+    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
   }
   if (sp.roll) {  // roll kernel geometry: 2 KiB steps, 16 steps per slice
     P->chunk_samples = kRollStep;
     P->slice_samples = static_cast<uint64_t>(kRollStep) * 16;
     P->back = best_halo;
     P->ring = kRollDepth;
-    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1;
+    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
   }
 
   // ---- shared-memory placement
@@ -813,7 +828,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     sp.table_in_smem = sp.verify_all ? 0 : 1;
     if (sp.direct)
       P->nwarps = best_warps ? best_warps
-                             : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps - 1) : kMaxWarps - 1);
+                             : (rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1);
   }
   sp.window_key = !sp.overlapping && !sp.verify_all && sp.q > 1;
   sp.wkey_len = sp.window_key ? static_cast<uint32_t>(std::min<size_t>(16, m - sp.q + 1)) : 0;
@@ -865,9 +880,17 @@ static inline uint64_t probe_entry(const ScanPlan& sp, uint32_t h, unsigned i) {
   return static_cast<uint64_t>(bloom_block(h, sp.blocks)) * 64 + bloom_bit(bloom_mix(h), i);
 }
 
+// Single-probe direct tables keep entry idx at bit (idx - 1) & 31 of word
+// idx >> 5: the kernel's wrap-mode funnel shift by idx lands it at bit 31
+// (scan_direct.cu rejects()).
+static inline bool rotated_entries(const Plan& P) { return P.sp.direct && P.sp.probes <= 1; }
+
 static inline void clear_bit(const Plan& P, std::vector<uint8_t>* t, uint64_t idx, unsigned b) {
   const unsigned el = P.sp.entry_log2;
-  if (el == 6) {
+  if (rotated_entries(P)) {
+    uint32_t* w = reinterpret_cast<uint32_t*>(t->data());
+    w[idx >> 5] &= ~(1u << ((idx - 1) & 31));
+  } else if (el == 6) {
     uint64_t* w = reinterpret_cast<uint64_t*>(t->data());
     w[idx] &= ~(1ull << b);
   } else {
@@ -880,6 +903,8 @@ static inline void clear_bit(const Plan& P, std::vector<uint8_t>* t, uint64_t id
 
 uint64_t mask_entry(const Plan& P, const std::vector<uint8_t>& t, uint64_t idx) {
   const unsigned el = P.sp.entry_log2;
+  if (rotated_entries(P))
+    return ((reinterpret_cast<const uint32_t*>(t.data())[idx >> 5] >> ((idx - 1) & 31)) & 1u) | ~1ull;
   if (el == 6) return reinterpret_cast<const uint64_t*>(t.data())[idx];
   const uint32_t* w = reinterpret_cast<const uint32_t*>(t.data());
   const uint64_t wi = idx >> (5 - el);
@@ -978,9 +1003,12 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   // L2 screen bitmap (window keys): top key bits
   pt->l2map.assign(sp.l2_bits ? std::max<size_t>(4, (size_t(1) << sp.l2_bits) / 32) : 4, 0);
   if (sp.l2_bits) {
+    // direct plans: bit b sits at (b - 1) & 31 of word b >> 5, so the kernel's
+    // rotate by the key lands it at bit 31 (scan_direct.cu resolve())
+    const uint32_t rot = sp.direct ? 31u : 0u;
     for (const Ent& e : ents) {
       const uint32_t b = screen_bit(e.key, sp.l2_bits);
-      pt->l2map[b >> 5] |= 1u << (b & 31);
+      pt->l2map[b >> 5] |= 1u << ((b + rot) & 31);
     }
   }
   // roll plans: open addressing by the start key, linear probing; patterns
@@ -1047,6 +1075,138 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
     pt->entries[2 * x] = e.key;
     pt->entries[2 * x + 1] = e.tag;
   }
+}
+
+double measure_candidates_per_byte(const Plan& P, const std::vector<uint8_t>& table,
+                                   const uint8_t* text, size_t n) {
+  const ScanPlan& sp = P.sp;
+  if (n == 0) return 0;
+  uint64_t cands = 0;
+  const uint32_t* w32 = reinterpret_cast<const uint32_t*>(table.data());
+  if (sp.verify_all) {
+    return 1.0;
+  } else if (sp.pack2) {  // level 1: the first 10 symbols' code
+    const unsigned sym = kPack2L1Bits / 2;
+    for (size_t p = 0; p + sym <= n; ++p) {
+      const uint32_t c = pack2_code(text + p, sym, sp.pack_shift);
+      cands += (w32[c >> 5] >> (c & 31)) & 1u;
+    }
+  } else if (sp.roll) {  // every position's q-byte prefix hash against its Bloom word
+    const uint32_t bq = roll_pow(sp.q);
+    uint32_t h = n >= sp.q ? roll_hash_bytes(text, sp.q) : 0;
+    for (size_t p = 0; p + sp.q <= n; ++p) {
+      const uint32_t wd = w32[roll_word(h * kRollMix, sp.roll_words)];
+      bool hit = true;
+      for (unsigned j = 0; j < sp.probes; ++j)
+        hit = hit && ((wd >> (31u - (roll_probe_shift(h, static_cast<int>(j)) & 31u))) & 1u);
+      cands += hit;
+      if (p + sp.q < n) h = h * kRollB + text[p + sp.q] - text[p] * bq;
+    }
+  } else {
+    // the Shift-Or machine of filter.hpp:58-73 (direct plans are its
+    // q = W, k = m' = 1 case): d = ((d << 1) & keep) | mask[gram]
+    uint64_t keep = ~0ull;
+    for (unsigned j = 0; j < sp.k; ++j) keep &= ~(1ull << (j * sp.m_prime));
+    const uint64_t T = filter_reads(P, n);
+    uint64_t d = ~0ull;
+    for (uint64_t t = 0; t < T; ++t) {
+      const uint64_t u = sp.overlapping ? t : (t + 1) * sp.k - 1;
+      const uint8_t* g = text + (sp.overlapping ? u : u * sp.q);
+      uint64_t mv;
+      if (sp.probes > 1) {
+        const uint32_t hh = hash_gram_bytes(g, sp.q);
+        mv = 0;
+        for (unsigned i = 0; i < sp.probes; ++i) mv |= mask_entry(P, table, probe_entry(sp, hh, i)) & 1ull;
+        mv |= ~1ull;
+      } else {
+        mv = mask_entry(P, table, gram_index_host(P, g));
+      }
+      d = ((d << 1) & keep) | mv;
+      cands += static_cast<uint64_t>(__builtin_popcountll(~d & sp.match_mask));
+    }
+  }
+  return static_cast<double>(cands) / static_cast<double>(n);
+}
+
+double measure_survivors_per_byte(const Plan& P, const PatternData& pd, const std::vector<uint8_t>& table,
+                                  const uint8_t* text, size_t n) {
+  const ScanPlan& sp = P.sp;
+  if (!sp.direct || n == 0) return 0;
+  // the screen of build_pattern_table: one bit per (pattern, shift) gram key
+  std::vector<uint32_t> screen(sp.l2_bits ? std::max<size_t>(4, (size_t(1) << sp.l2_bits) / 32) : 0, 0);
+  if (sp.l2_bits)
+    for (size_t i = 0; i < pd.r; ++i)
+      for (unsigned s = 0; s < sp.q; ++s) {
+        const uint32_t b = screen_bit(hash_gram_bytes(pd.pattern(i) + s, sp.q), sp.l2_bits);
+        screen[b >> 5] |= 1u << (b & 31);
+      }
+  uint64_t surv = 0;
+  for (uint64_t t = 0; t < n / sp.q; ++t) {
+    const uint32_t h = hash_gram_bytes(text + t * sp.q, sp.q);
+    bool hit = true;
+    if (sp.probes > 1) {
+      for (unsigned i = 0; i < sp.probes; ++i) hit = hit && !(mask_entry(P, table, probe_entry(sp, h, i)) & 1ull);
+    } else {
+      hit = !(mask_entry(P, table, gram_slot(h, sp.table_bits)) & 1ull);
+    }
+    if (!hit) continue;
+    const uint32_t b = screen_bit(h, sp.l2_bits);
+    surv += sp.l2_bits ? (screen[b >> 5] >> (b & 31)) & 1u : 1u;
+  }
+  return static_cast<double>(surv) / static_cast<double>(n);
+}
+
+int make_plan_measured(const PatternData& pd, const Histogram& h, const PlanRequest& rq,
+                       const uint8_t* sample, size_t sample_len, Plan* P, std::string* err) {
+  const int rc = make_plan(pd, h, rq, P, err);
+  if (rc != 0 || !sample || sample_len < 4096 || sample_len < 4 * pd.m) return rc;
+  const size_t n = std::min<size_t>(sample_len, size_t(1) << 20);
+  auto measure = [&](Plan* pl) {
+    std::vector<uint8_t> table;
+    build_masks(*pl, pd, &table);
+    pl->meas_cand_per_byte = measure_candidates_per_byte(*pl, table, sample, n);
+    pl->meas_sample_bytes = n;
+    double cost = pl->pred_cost + pl->cost_slope * (pl->meas_cand_per_byte - pl->pred_cand_per_byte);
+    if (pl->sp.direct) {
+      pl->meas_surv_per_byte = measure_survivors_per_byte(*pl, pd, table, sample, n);
+      cost += pl->surv_slope * (pl->meas_surv_per_byte - pl->pred_surv_per_byte);
+    }
+    pl->meas_cost = std::max(0.0, cost);
+  };
+  measure(P);
+  P->meas_plans = 1;
+  // pinned plans are only measured: reference parameters, a forced kernel,
+  // fixed q / table / probes / ring options
+  const bool pinned = P->sp.gram_mode == kGramExact || rq.kernel != 0 || rq.q || rq.k || rq.table_bits ||
+                      rq.probes || rq.stages || rq.tile_bytes || rq.variant == 1;
+  if (pinned) return rc;
+  struct Family {
+    int kernel, q;
+  };
+  static const Family kFamilies[] = {{1, 0}, {2, 16}, {2, 8}, {3, 0}};
+  Plan best = *P;
+  uint32_t measured = 1;
+  for (const Family& f : kFamilies) {
+    PlanRequest r2 = rq;
+    r2.kernel = f.kernel;
+    r2.gram_mode = 1;  // a fixed q would otherwise select the reference's exact-code path
+    r2.q = f.q;
+    Plan alt;
+    std::string e2;
+    if (make_plan(pd, h, r2, &alt, &e2) != 0) continue;
+    const bool same = alt.sp.direct == P->sp.direct && alt.sp.roll == P->sp.roll && alt.sp.q == P->sp.q &&
+                      alt.sp.k == P->sp.k && alt.sp.m_prime == P->sp.m_prime &&
+                      alt.sp.table_bits == P->sp.table_bits && alt.sp.probes == P->sp.probes &&
+                      alt.sp.overlapping == P->sp.overlapping && alt.sp.verify_all == P->sp.verify_all;
+    if (same) continue;
+    measure(&alt);
+    ++measured;
+    // a clear margin: the calibrated analytic choice stands on near ties
+    if (alt.meas_cost < 0.9 * best.meas_cost) best = alt;
+  }
+  *P = best;
+  P->meas_plans = measured;
+  return rc;
 }
 
 uint64_t filter_reads(const Plan& P, uint64_t n) {

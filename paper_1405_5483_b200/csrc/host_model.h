@@ -93,6 +93,17 @@ struct Plan {
   uint32_t slot_bytes = 0;
   uint32_t ring = 0, nwarps = 0;
   double pred_cand_per_byte = 0;
+  // planner's cost (thread-instructions per text byte) and its derivative in
+  // the candidate rate: a measured rate re-prices the plan as
+  // pred_cost + cost_slope * (measured - predicted)
+  double pred_cost = 0, cost_slope = 0;
+  // direct plans: filter hits that also pass the L2 screen walk a bucket
+  // (true gram matches of repetitive text all do); priced separately
+  double pred_surv_per_byte = 0, surv_slope = 0, meas_surv_per_byte = -1;
+  // measured on a text sample (mag_options.histogram_sample): -1 = no sample
+  double meas_cand_per_byte = -1, meas_cost = 0;
+  uint64_t meas_sample_bytes = 0;
+  uint32_t meas_plans = 0;  // finalist plans whose filters ran over the sample
 };
 
 size_t plan_smem(const Plan& p);
@@ -100,6 +111,25 @@ size_t plan_smem(const Plan& p);
 // Errors: returns a mag_status value (0 ok) and fills *err.
 int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, Plan* plan,
               std::string* err);
+
+// GPU-aware parameter choice with measured candidate rates (
+// replaces the uniform-text estimate of tuner.hpp:58-66 where a text sample
+// is given): make_plan, then the analytic best plan of every kernel family
+// has its real filter table built and run over `sample`; the measured
+// candidates per byte re-price each plan and the cheapest one is returned.
+// Plans the caller pinned (reference parameters, a forced kernel) are
+// measured but not replaced.
+int make_plan_measured(const PatternData& pd, const Histogram& h, const PlanRequest& rq,
+                       const uint8_t* sample, size_t sample_len, Plan* plan, std::string* err);
+
+// The plan's own filter over text[0, n): candidates per text byte, counted
+// as the kernels count mag_metrics.candidates.
+double measure_candidates_per_byte(const Plan& plan, const std::vector<uint8_t>& table,
+                                   const uint8_t* text, size_t n);
+// Direct plans: filter hits per byte that also pass the L2 screen bitmap
+// (built here from the patterns' (pattern, shift) gram keys).
+double measure_survivors_per_byte(const Plan& plan, const PatternData& pd, const std::vector<uint8_t>& table,
+                                  const uint8_t* text, size_t n);
 
 // Packed mask table (bit j*m'+i of entry c is 0 iff c admitted at alignment
 // j position i; filter.hpp:27-31), table_bytes long.

@@ -16,15 +16,12 @@
 namespace magb {
 namespace {
 
-// Read-only load under a predicate (0 when off): one predicated LDG, no branch.
-__device__ __forceinline__ uint32_t ld_nc_pred(const uint32_t* p, bool on) {
-  uint32_t v;
-  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\tmov.u32 %0, 0;\n\t"
-      "@q ld.global.nc.u32 %0, [%1];\n\t}"
-      : "=r"(v)
-      : "l"(p), "r"(static_cast<uint32_t>(on)));
-  return v;
-}
+// Diagnostics builds only (MAG_B200_DIAG): stage-skip bits of the plan.
+#ifdef MAG_B200_DIAGNOSTICS
+#define MAG_DIAG(A, bits) ((A).plan.diag & (bits))
+#else
+#define MAG_DIAG(A, bits) 0
+#endif
 
 // Multi-probe membership on a 64-entry block given as two words.
 template <int H>
@@ -63,9 +60,11 @@ struct DirectScanner {
   static constexpr uint32_t kStepBytes = W == 16 ? 4096u : 2048u;
   static constexpr uint32_t kStep = kStepBytes / W;
   static constexpr int kPer = kStep / 32;  // samples per lane per step
-  // screen loads in flight: word and key (the key's low 5 bits are its
-  // screen bit within the word: l2_bits >= 16)
-  uint32_t pend_w[kPer], pend_k[kPer], pend_pos;
+  // screen loads in flight: word and key (the key's low bits rotate its
+  // screen bit to bit 31: l2_bits >= 16), and the step's filter-hit mask
+  // (sample i at bit kPer - 1 - i)
+  uint32_t pend_w[kPer], pend_k[kPer], pend_m, pend_pos;
+  const uint32_t tshift, wmask;  // 32 - table_bits; screen words - 1
   // producer cursor (warp-uniform)
   unsigned long long p_t;
   uint32_t p_left;
@@ -75,8 +74,10 @@ struct DirectScanner {
   __device__ DirectScanner(const ScanArgs& a, const void* tab, uint2* q, uint8_t* sl, uint64_t* b, DirectDesc* dsc,
                            int l)
       : A(a), lane(l), table(tab), pq(q), slots(sl), bars(b), desc(dsc), pqn(0), fill(0), cands32(0),
-        cur_slice(0), out(nullptr), p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
+        cur_slice(0), out(nullptr), tshift(32u - a.plan.table_bits), wmask((1u << (a.plan.l2_bits - 5)) - 1u),
+        p_t(0), p_left(0), p_done(false), pol(policy_evict_first()) {
     for (int i = 0; i < kPer; ++i) pend_w[i] = pend_k[i] = 0;
+    pend_m = 0;
     pend_pos = 0;
   }
 
@@ -137,20 +138,23 @@ struct DirectScanner {
     }
   }
 
-  __device__ __forceinline__ bool admits(uint32_t h) const {
+  // Table lookup of a gram hash: bit 31 of the result is SET when the gram
+  // is not admitted.  Single-probe tables keep entry idx at bit (idx - 1) & 31
+  // of word idx >> 5 (host_model.cpp clear_bit), so one wrap-mode funnel
+  // shift by idx lands it at bit 31, where a second funnel shift collects it.
+  __device__ __forceinline__ uint32_t rejects(uint32_t h) const {
     if constexpr (H > 1) {
       const uint2 blk = static_cast<const uint2*>(table)[bloom_block(h, A.plan.blocks)];
-      return bloom_admits_w<H>(blk.x, blk.y, h);
+      return bloom_admits_w<H>(blk.x, blk.y, h) ? 0u : 0x80000000u;
     } else {
-      // word h >> (37 - tb), bit (h >> (32 - tb)) & 31 via a wrap-mode funnel shift
-      const uint32_t idx = h >> (32 - A.plan.table_bits);
+      const uint32_t idx = h >> tshift;
       const uint32_t wd = static_cast<const uint32_t*>(table)[idx >> 5];
-      return !(__funnelshift_r(wd, wd, idx) & 1u);
+      return __funnelshift_r(wd, wd, idx);
     }
   }
 
   __device__ __forceinline__ void flush() {
-    if (!(A.plan.diag & 16))
+    if (!MAG_DIAG(A, 16))
       fill = flush_queue(A, pq, pqn, W * slice_t0(A, cur_slice), out, fill, lane, true);
     pqn = 0;
   }
@@ -168,54 +172,47 @@ struct DirectScanner {
   // Filter the lane's kPer samples of a step; a filter hit issues its L2
   // screen load now and is resolved one step later (resolve()), so the L2
   // round trip overlaps the next step's filtering instead of stalling.
+  // Straight-line code: the hit bits are collected into one mask by funnel
+  // shifts, and every sample issues its screen load — a miss loads word 0
+  // (one L1-resident address for the whole warp) and is masked off in
+  // resolve().  Per sample: hash 7, lookup 6, screen 5 instructions.
   __device__ __forceinline__ void filter(const uint32_t (&h)[kPer], uint32_t lim) {
-    const uint32_t lb = A.plan.l2_bits;
-    const bool count_only = A.plan.diag & 8;  // diagnostics: no screen / verification
-    const bool screen = lb && !(A.plan.diag & 128);
-    bool hit[kPer];
+    uint32_t rej = 0;
     // all lookups first (independent shared-memory loads in flight together)
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) hit[i] = admits(h[i]);
+    for (int i = 0; i < kPer; ++i) rej = __funnelshift_l(rejects(h[i]), rej, 1);
+    uint32_t m = ~rej & ((1u << kPer) - 1u);
     if (lim < kStep) {  // the text's last step: samples past the end never hit
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) hit[i] = hit[i] && static_cast<uint32_t>(lane + 32 * i) < lim;
+      for (int i = 0; i < kPer; ++i)
+        if (static_cast<uint32_t>(lane + 32 * i) >= lim) m &= ~(1u << (kPer - 1 - i));
     }
+    cands32 += __popc(m);
+    if (MAG_DIAG(A, 8)) m = 0;  // diagnostics: no screen / verification
+    pend_m = m;
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-      cands32 += hit[i] ? 1u : 0u;
       // the window key is the sample's gram hash (direct plans: key_gram)
       const uint32_t key = h[i];
       pend_k[i] = key;
-      const uint32_t sb = lb ? screen_bit(key, lb) : 0u;  // resolve() shifts by key: bit sb & 31
-      // the screen word is only consumed by resolve() one step later.  W = 16
-      // plans (a quarter to most samples hit: cfg2/cfg4) issue it as one
-      // predicated load, no branch per sample (cfg2 +5%); W = 8 plans (rare
-      // hits: cfg1/cfg3) branch around it, which skips whole warps
-      const bool want = hit[i] && !count_only;
-      uint32_t w;
-      if constexpr (W == 16) {
-        if (screen)
-          w = ld_nc_pred(A.l2map + (sb >> 5), want);
-        else
-          w = want ? ~0u : 0u;
-      } else {
-        w = 0;
-        if (want) w = screen ? __ldg(A.l2map + (sb >> 5)) : ~0u;
-      }
-      pend_w[i] = w;
+      const uint32_t wi = (m >> (kPer - 1 - i)) & 1u ? (key >> 5) & wmask : 0u;
+      pend_w[i] = __ldg(A.l2map + wi);
     }
   }
 
+  // The previous step's screen words: bit screen_bit(key) of the map sits at
+  // bit (key - 1) & 31 of its word (host_model.cpp, direct plans), so a
+  // rotate by key brings it to bit 31.
   __device__ __forceinline__ void resolve() {
-    uint32_t surv = 0;
+    uint32_t s = 0;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) surv |= (__funnelshift_r(pend_w[i], pend_w[i], pend_k[i]) & 1u) << i;
-    if (__any_sync(kFull, surv != 0)) {
+    for (int i = 0; i < kPer; ++i) s = __funnelshift_l(__funnelshift_r(pend_w[i], pend_w[i], pend_k[i]), s, 1);
+    s &= pend_m;
+    pend_m = 0;
+    if (__any_sync(kFull, s != 0)) {
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) push((surv >> i) & 1u, pend_k[i], pend_pos + 32u * W * i);
+      for (int i = 0; i < kPer; ++i) push((s >> (kPer - 1 - i)) & 1u, pend_k[i], pend_pos + 32u * W * i);
     }
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) pend_w[i] = 0;
   }
 
   // Step prologue (independent of the step's data: runs while its
@@ -237,7 +234,7 @@ struct DirectScanner {
     // sample offset within the slice (slices < 2^32 samples; low words suffice)
     pend_pos = W * (d.t_lo - static_cast<uint32_t>(slice_t0(A, cur_slice))) + W * lane;
     filter(h, lim);
-    if (A.plan.diag & 64) resolve();  // diagnostics: no cross-step deferral
+    if (MAG_DIAG(A, 64)) resolve();  // diagnostics: no cross-step deferral
     if (flags & 2u) {
       resolve();
       if (pqn) flush();
@@ -355,6 +352,8 @@ cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, si
 }  // namespace
 
 cudaError_t launch_direct(const ScanArgs& a, cudaStream_t stream, int grid) {
+  // every direct plan screens its window keys (host_model.cpp: l2_bits >= 16)
+  if (a.plan.l2_bits < 16 || a.plan.l2_bits > 32) return cudaErrorInvalidValue;
   const size_t smem = direct_smem(a.plan, a.nwarps);
   switch (a.plan.probes) {
     case 1: return launch_direct_h<1>(a, stream, grid, smem);
