@@ -66,8 +66,7 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, int lane) {
 // 16 pattern bytes at a time against two aligned 16-byte text loads
 // (independent, one round trip per piece) realigned with funnel shifts.
 __device__ __forceinline__ uint32_t fsr(uint32_t lo, uint32_t hi, uint32_t b) { return __funnelshift_r(lo, hi, b); }
-__device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len) {
-  const uint8_t* p = A.pat_bytes + __ldg(A.pat_off + pid);
+__device__ bool equal_text_p(const ScanArgs& A, unsigned long long a, const uint8_t* p, uint32_t len) {
   if (a + len + 32 > A.n) {  // near the end of the text: bytewise (no over-read)
     const uint8_t* t = A.text + a;
     for (uint32_t i = 0; i < len; ++i)
@@ -101,12 +100,19 @@ __device__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid
   return true;
 }
 
+__device__ __forceinline__ bool equal_text(const ScanArgs& A, unsigned long long a, uint32_t pid, uint32_t len) {
+  return equal_text_p(A, a, A.pat_bytes + __ldg(A.pat_off + pid), len);
+}
+
 // Window-key bucket walk: a candidate window's key (read at its gram
 // boundary a0) against the (pattern, shift) index; entry shift s names the
 // start a0 - s.  Entries come in (shift descending, pattern ascending) order
-// = text order.  Counted, or written (dst != nullptr) from dst[idx].
+// = text order.  Counted (the first match kept in *first), or written
+// (dst != nullptr) from dst[idx].  A pattern's length and offset are loaded
+// together, so a hit costs four dependent round trips: bucket bounds, entry,
+// {length, offset}, {text, pattern bytes}.
 __device__ uint32_t window_probe(const ScanArgs& A, unsigned long long a0, uint32_t key, uint64_t* dst,
-                                 uint32_t idx) {
+                                 uint32_t idx, uint64_t* first = nullptr) {
   const uint32_t b = key & ((1u << A.plan.bucket_bits) - 1u);
   const uint32_t lo = __ldg(A.bucket_start + b), hi = __ldg(A.bucket_start + b + 1);
   uint32_t c = 0;
@@ -117,8 +123,13 @@ __device__ uint32_t window_probe(const ScanArgs& A, unsigned long long a0, uint3
     if (s > a0) continue;
     const unsigned long long a = a0 - s;
     const uint32_t len = __ldg(A.pat_len + pid);
-    if (a + len > A.n || !equal_text(A, a, pid, len)) continue;
-    if (dst && idx + c < A.slice_cap) dst[idx + c] = pack_match(a, pid);
+    const uint64_t off = __ldg(A.pat_off + pid);
+    if (a + len > A.n || !equal_text_p(A, a, A.pat_bytes + off, len)) continue;
+    if (dst) {
+      if (idx + c < A.slice_cap) dst[idx + c] = pack_match(a, pid);
+    } else if (first && c == 0) {
+      *first = pack_match(a, pid);
+    }
     ++c;
   }
   return c;
@@ -164,11 +175,19 @@ __device__ __noinline__ uint32_t flush_queue(const ScanArgs& A, uint2* pq, uint3
     const uint32_t i = i0 + lane;
     uint2 e = make_uint2(0u, 0xffffffffu);
     uint32_t c = 0;
+    uint64_t first = 0;
     if (i < nlive) {
       e = pq[i];
-      c = window_probe(A, pbase + e.y, e.x, nullptr, 0);
+      c = window_probe(A, pbase + e.y, e.x, nullptr, 0, &first);
     }
     if (!__any_sync(kFull, c != 0)) continue;
+    if (!__any_sync(kFull, c > 1)) {  // at most one match per key (the common case): one pass
+      const unsigned one = __ballot_sync(kFull, c == 1);
+      const uint32_t at = fill + __popc(one & ((1u << lane) - 1u));
+      if (c && at < A.slice_cap) out[at] = first;
+      fill += __popc(one);
+      continue;
+    }
     const uint32_t excl = warp_excl_scan(c, lane);
     const uint32_t total = __shfl_sync(kFull, excl + c, 31);
     if (c) window_probe(A, pbase + e.y, e.x, out, fill + excl);
