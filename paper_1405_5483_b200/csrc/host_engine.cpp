@@ -246,7 +246,7 @@ uint64_t bytes_per_sample(const Plan& P) {
 
 uint64_t step_unit(const Plan& P) {
   if (P.sp.pack2) return kPack2Step;
-  return P.sp.roll ? kRollStep : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);
+  return P.sp.roll ? P.sp.roll_step : (P.sp.direct ? direct_step_bytes(P.sp.q) / P.sp.q : P.chunk_samples);
 }
 
 // Slices are the warps' work items: the plan's size, but small texts get

@@ -358,6 +358,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
   const unsigned w = rq.word_bits > 0 ? std::min(64, rq.word_bits) : 64;
 
   uint32_t best_halo = 0;   // roll plans: staged bytes past a step
+  uint32_t best_roll_warps = 0, best_roll_step = kRollStep;
   uint32_t best_warps = 0;  // direct plans: warps per CTA the planner chose
   const bool reference_mode = rq.gram_mode == 0 ||
                               (rq.gram_mode < 0 && (rq.q || rq.k || rq.sigma_prime ||
@@ -642,11 +643,18 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           q = c;
           break;
         }
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
+      // equal-length sets of <= 12 bytes run the pipelined kernel: up to 24 warps
+      const bool eq_set = pd.maxlen == pd.m && pd.m <= 12;
+      // (cfg5, 15 / 16 / 20 warps: 690 / 718 / 655 GB/s; the finish grid waits for a CTA to leave)
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, eq_set ? kRollMaxWarps : kMaxWarps)
+                                          : (eq_set ? kMaxWarps : kMaxWarps - 1);
+      best_roll_warps = warps;
       const uint32_t v4 = (32 + q - 1 + 15) / 16;
       const uint32_t halo = static_cast<uint32_t>(
           align16(std::max<size_t>(16 * v4, std::min<size_t>(pd.maxlen, 240) + 8)));
-      const size_t fixed = roll_smem(0, halo, warps) + 1024;
+      const uint32_t rstep = eq_set ? kRollStepEq : kRollStep;
+      best_roll_step = rstep;
+      const size_t fixed = roll_smem(0, halo, warps, rstep) + 1024;
       // Bloom words: what shared memory leaves, but no more than ~2 Kibit per
       // pattern (every CTA loads the table: small sets keep it small)
       const size_t room_words = rq.smem_limit > fixed ? (rq.smem_limit - fixed) / 16 * 4 : 0;
@@ -661,7 +669,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
         const double fp = std::min(1.0, 1.4 * std::pow(fill, static_cast<double>(H)));  // blocked penalty
         const double cpb = exact + (1.0 - exact) * fp;
         // a step (2048 positions) with any hit pays one verification batch
-        const double batch = 1.0 - std::exp(-cpb * kRollStep);
+        const double batch = 1.0 - std::exp(-cpb * rstep);
         const double cost = kCostRollPos + H * kCostRollProbe + kCostRollWarm * q / 32.0 + cpb * kCostRollCand +
                             batch * kCostRollBatch;
         if (cost < best.cost * 0.999) {
@@ -676,7 +684,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
           best.roll = 1;
           best.roll_words = words;
           best.halo = halo;
-          best.chunk = kRollStep;
+          best.chunk = rstep;
         }
       }
     }
@@ -806,11 +814,12 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
   }
   if (sp.roll) {  // roll kernel geometry: 2 KiB steps, 16 steps per slice
-    P->chunk_samples = kRollStep;
-    P->slice_samples = static_cast<uint64_t>(kRollStep) * 16;
+    sp.roll_step = best_roll_step;
+    P->chunk_samples = best_roll_step;
+    P->slice_samples = 32768;  // whole steps either way
     P->back = best_halo;
     P->ring = kRollDepth;
-    P->nwarps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
+    P->nwarps = best_roll_warps ? best_roll_warps : kMaxWarps - 1;
   }
 
   // ---- shared-memory placement
@@ -860,7 +869,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
 size_t plan_smem(const Plan& p) {
   if (p.sp.direct) return direct_smem(p.sp, p.nwarps);
   if (p.sp.pack2) return pack2_smem(p.sp.table_bytes, p.back, p.nwarps);
-  if (p.sp.roll) return roll_smem(p.sp.roll_words, p.back, p.nwarps);
+  if (p.sp.roll) return roll_smem(p.sp.roll_words, p.back, p.nwarps, p.sp.roll_step);
   return smem_layout(p.sp, p.slot_bytes, p.ring, p.nwarps).total;
 }
 
@@ -1041,27 +1050,81 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
       if (pt->vtab[8 * i + 1] != 0xffffffffu && pt->vtab[8 * ((i + 1) & pt->vmask) + 1] != 0xffffffffu)
         pt->vtab[8 * i + 2] |= 0x80000000u;
   }
-  if (sp.roll) {
+  if (sp.roll && sp.roll_step == static_cast<uint32_t>(kRollStepEq)) {
+    // Equal-length sets of m <= 12 bytes: 32-byte sectors of two 16-byte
+    // entries {pattern (zero padded to 12 bytes), pid | F << 31}; empty
+    // entries have the pid word 0xffffffff.  Pass 1 places every pattern in
+    // its home sector while that has room (id order: entry 0 before entry
+    // 1); pass 2 moves the others to the next sector with room and sets F
+    // in the HOME sector's entry 0: "patterns of this home live further
+    // along" — the only case in which the kernel walks on (~1.6% of the
+    // patterns at <= 0.25 patterns per sector).
+    size_t sectors = 16;
+    while (sectors < 4 * r) sectors <<= 1;
+    pt->vmask = static_cast<uint32_t>(sectors - 1);
+    pt->vtab.assign(8 * sectors, 0);
+    for (size_t i = 0; i < 2 * sectors; ++i) pt->vtab[4 * i + 3] = 0xffffffffu;
+    auto put = [&](size_t sec, size_t i) -> bool {
+      for (int e = 0; e < 2; ++e) {
+        uint32_t* w = &pt->vtab[8 * sec + 4 * e];
+        if (w[3] != 0xffffffffu) continue;
+        std::memcpy(w, pd.pattern(i), 12);  // patterns are zero padded to 16 bytes
+        w[3] = static_cast<uint32_t>(i);
+        return true;
+      }
+      return false;
+    };
+    std::vector<uint8_t> placed(r, 0);
+    std::vector<uint32_t> keys(r);
+    for (size_t i = 0; i < r; ++i) {
+      keys[i] = key_bytes(pd.pattern(i), sp.key_len);
+      placed[i] = put(keys[i] & pt->vmask, i);
+    }
+    for (size_t i = 0; i < r; ++i) {
+      if (placed[i]) continue;
+      const size_t home = keys[i] & pt->vmask;
+      size_t sec = home;
+      do sec = (sec + 1) & pt->vmask; while (!put(sec, i));
+      pt->vtab[8 * home + 3] |= 0x80000000u;
+    }
+  } else if (sp.roll) {
     size_t slots = 16;
     while (slots < 4 * r) slots <<= 1;  // load factor <= 1/4
     pt->vmask = static_cast<uint32_t>(slots - 1);
     pt->vtab.assign(8 * slots, 0);
     for (size_t i = 0; i < slots; ++i) pt->vtab[8 * i + 1] = 0xffffffffu;
-    for (size_t i = 0; i < r; ++i) {
-      const uint32_t key = key_bytes(pd.pattern(i), sp.key_len);
-      size_t s = key & pt->vmask;
-      while (pt->vtab[8 * s + 1] != 0xffffffffu) s = (s + 1) & pt->vmask;
-      uint32_t* e = &pt->vtab[8 * s];
-      e[0] = key;
+    auto put = [&](size_t s, size_t i, uint32_t key) {
+      uint32_t* e = &pt->vtab[8 * s];  // {len | F << 31, pid, key, pattern offset / 16}
+      e[0] = pd.len[i];
       e[1] = static_cast<uint32_t>(i);
-      e[2] = pd.len[i];
+      e[2] = key;
       e[3] = static_cast<uint32_t>(pd.off[i] / 16);
       std::memcpy(e + 4, pd.pattern(i), 16);  // patterns are zero padded to 16 bytes
+    };
+    // Pass 1: every home slot goes to the first (lowest id) pattern that
+    // hashes there, so a lookup of a key whose home holds one pattern is ONE
+    // L2 round trip.  Pass 2: the others, in id order, probe linearly from
+    // their home (equal keys are therefore met in id order along a run) and
+    // set bit 31 of their HOME slot's len word: "patterns of this home live
+    // further along" — the only case in which the kernel walks on.
+    std::vector<uint32_t> keys(r);
+    std::vector<uint8_t> placed(r, 0);
+    for (size_t i = 0; i < r; ++i) {
+      keys[i] = key_bytes(pd.pattern(i), sp.key_len);
+      const size_t s = keys[i] & pt->vmask;
+      if (pt->vtab[8 * s + 1] == 0xffffffffu) {
+        put(s, i, keys[i]);
+        placed[i] = 1;
+      }
     }
-    // bit 31 of the len word: the next slot is occupied (the probe run goes on)
-    for (size_t i = 0; i < slots; ++i)
-      if (pt->vtab[8 * i + 1] != 0xffffffffu && pt->vtab[8 * ((i + 1) & pt->vmask) + 1] != 0xffffffffu)
-        pt->vtab[8 * i + 2] |= 0x80000000u;
+    for (size_t i = 0; i < r; ++i) {
+      if (placed[i]) continue;
+      const size_t home = keys[i] & pt->vmask;
+      size_t s = home;
+      while (pt->vtab[8 * s + 1] != 0xffffffffu) s = (s + 1) & pt->vmask;
+      put(s, i, keys[i]);
+      pt->vtab[8 * home] |= 0x80000000u;
+    }
   }
   // buckets by low key bits, stable within a bucket
   const size_t nb = size_t(1) << sp.bucket_bits;

@@ -143,7 +143,8 @@ struct PatternTable {
   std::vector<uint32_t> bucket_start;
   std::vector<uint32_t> entries;  // interleaved key, pid
   // roll plans: open-addressing verification table, 8 words per slot
-  // {key, pid (0xffffffff = empty), len, pattern offset / 16, first 16 bytes}
+  // {len | F << 31, pid (0xffffffff = empty), key, pattern offset / 16, first 16 bytes};
+  // F: patterns whose home slot this is live further along the probe run
   std::vector<uint32_t> vtab;
   uint32_t vmask = 0;
   uint32_t vbits = 0;  // pack2: log2 slots

@@ -14,6 +14,14 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Diagnostics builds only (-DMAG_B200_DIAGNOSTICS, MAG_B200_DIAG): stage-skip
+// bits of the plan; product builds compile the checks away.
+#ifdef MAG_B200_DIAGNOSTICS
+#define MAG_DIAG(A, bits) ((A).plan.diag & (bits))
+#else
+#define MAG_DIAG(A, bits) 0
+#endif
+
 // ------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

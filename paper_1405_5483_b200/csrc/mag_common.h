@@ -152,6 +152,7 @@ struct ScanPlan {
   uint32_t ddepth;        // direct: TMA ring depth per warp (0 = kDirectDepth)
   int roll;               // dense rolling-hash scan: every position, q-gram Bloom
   uint32_t roll_words;    // roll: 32-bit Bloom words (table_bytes = 4 * roll_words)
+  uint32_t roll_step;     // roll: positions per step (kRollStepEq for equal-length short sets, else kRollStep)
   int pack2;              // dense 2-bit-code scan (<= 4 pattern symbols): every position
   uint32_t pack_shift;    // pack2: symbol map b -> (b >> pack_shift) & 3
   uint32_t vbits;         // pack2: log2 level-2 slots
@@ -226,12 +227,16 @@ MAG_HD size_t direct_smem(const ScanPlan& p, uint32_t nwarps) {
 // Roll kernel: Bloom words, per-warp ring of kRollDepth slots of
 // kRollStep text bytes + halo (+ mbarriers and step descriptors).
 constexpr int kRollDepth = 2;
+constexpr int kRollMaxWarps = 24;  // equal-length short sets (80-register kernel); others: kMaxWarps
 constexpr int kRollStep = 2048;   // positions per step: 2 runs of 32 per lane
-MAG_HD uint32_t roll_slot_bytes(uint32_t halo) { return static_cast<uint32_t>(align16(kRollStep + halo)); }
+constexpr int kRollStepEq = 1024; // equal-length short sets: 1 run per lane (pipelined verification)
+MAG_HD uint32_t roll_slot_bytes(uint32_t step, uint32_t halo) { return static_cast<uint32_t>(align16(step + halo)); }
 constexpr int kRollList = 256;     // per-warp list of a step's hit positions (u16)
-MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps) {
-  return align16(size_t(words) * 4) + size_t(nwarps) * kRollDepth * roll_slot_bytes(halo) +
-         size_t(nwarps) * kRollDepth * (32 + 8) + size_t(nwarps) * kRollList * 2 + 64;
+constexpr int kRollListEq = 128;
+MAG_HD size_t roll_smem(uint32_t words, uint32_t halo, uint32_t nwarps, uint32_t step) {
+  return align16(size_t(words) * 4) + size_t(nwarps) * kRollDepth * roll_slot_bytes(step, halo) +
+         size_t(nwarps) * kRollDepth * (32 + 8) +
+         size_t(nwarps) * (step == static_cast<uint32_t>(kRollStepEq) ? kRollListEq : kRollList) * 2 + 64;
 }
 
 // Pack2 kernel: 2^20-bit level-1 bitmap, per-warp ring of kPack2Depth slots

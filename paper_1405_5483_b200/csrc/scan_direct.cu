@@ -16,13 +16,6 @@
 namespace magb {
 namespace {
 
-// Diagnostics builds only (MAG_B200_DIAG): stage-skip bits of the plan.
-#ifdef MAG_B200_DIAGNOSTICS
-#define MAG_DIAG(A, bits) ((A).plan.diag & (bits))
-#else
-#define MAG_DIAG(A, bits) 0
-#endif
-
 // Multi-probe membership on a 64-entry block given as two words.
 template <int H>
 __device__ __forceinline__ bool bloom_admits_w(uint32_t lo, uint32_t hi, uint32_t h) {

@@ -14,7 +14,7 @@ for c in ${CFGS:-2 3 4 5 1}; do
   P="python tools/profile_run.py --config $c --iters 1 ${PROF_OPTS:+--opts $PROF_OPTS}"
   R=gpurun_out/full_cfg$c${TAG}
   $P > gpurun_out/plain_cfg$c.log 2>&1 &&
-  ncu --set full --clock-control none --import-source on -k regex:'mag_(direct|scan)_kernel' -s 2 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:'mag_(direct|scan|roll|pack2)_kernel' -s 2 -c 1 \
       -o $R $P > gpurun_out/ncu_full_cfg$c.log 2>&1
   tail -2 gpurun_out/ncu_full_cfg$c.log
   ncu -i $R.ncu-rep --page raw --csv > $R.raw.csv 2>/dev/null
