@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
       }
       const uint32_t excl = u - cnt, tot = __shfl_sync(kFull, u, 31);
       if (!tot) continue;
-      constexpr int kU = 8;
+      constexpr int kU = 16;  // loads in flight per lane (8 -> 16: cfg5 finish 0.15 -> ? ms)
       if (!__any_sync(kFull, cnt > A.slice_cap)) {
         // element e belongs to the last slice whose exclusive prefix is <= e
         for (uint32_t e0 = 0; e0 < tot; e0 += 32 * kU) {

@@ -33,6 +33,7 @@ e = mag.Engine(w.patterns, **kw)
 d = torch.from_numpy(w.text).cuda()
 p = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
 s = torch.cuda.Stream()
+e.search_prepared(p).close()  # materialised once: the engine learns the staging capacity per slice
 for _ in range(2):  # warm-up: lazy module load, workspace allocation
     e.search_prepared_async(p, s.cuda_stream).close()
 torch.cuda.synchronize()
