@@ -243,7 +243,7 @@ def config_sweep(cells, local, steps=10, warmup=3):
             torch.cuda.empty_cache()
             cache[c] = workloads.generate(c, 1.0)
         w = cache[c]
-        eng = mag.Engine(w.patterns, device=local, **kw)
+        eng = mag.Engine(w.patterns, device=local, histogram_sample=w.text[:1 << 20], **kw)
         d = torch.from_numpy(w.text).to(f"cuda:{local}")
         prep = eng.prepare_device(d.data_ptr(), w.text.size, keep=d)
         m = eng.search_prepared(prep)
@@ -276,18 +276,29 @@ def config_sweep(cells, local, steps=10, warmup=3):
                 torch.cuda.synchronize()
                 ms += e0.elapsed_time(e1)
         kms, kl = mag.scan_timer_read()
+        mag.scan_timer(True, scan_only=True)  # the scan kernel alone
+        with torch.cuda.stream(st):
+            for _ in range(steps):
+                if flush is not None:
+                    flush.sum()
+                eng.search_prepared_async(prep, st.cuda_stream).close()
+        torch.cuda.synchronize()
+        sms, sl = mag.scan_timer_read()
         mag.scan_timer(False)
         n = int(w.text.size)
         step_gbs = n / (ms / steps * 1e-3) / 1e9
         kern_gbs = n / (kms / max(kl, 1) * 1e-3) / 1e9
+        scan_gbs = n / (sms / max(sl, 1) * 1e-3) / 1e9
         pl = eng.plan()
         out[f"cfg{c}{label}"] = {
             "workload": w.name, "n": n, "r": len(w.patterns), "GB/s": step_gbs, "kernel_GB/s": kern_gbs,
+            "scan_kernel_GB/s": scan_gbs, "scan_frac_of_hbm": scan_gbs / peak,
             "frac_of_hbm": kern_gbs / peak, "step_frac_of_hbm": step_gbs / peak, "matches": int(offs.size),
             "filter_reads": met.filter_reads, "candidates": met.candidates, "bit_exact_vs_reference": bool(ok),
             "l2": "read-only 256 MiB pass between steps" if flush is not None else "input larger than L2",
             "plan": {k: pl[k] for k in ("variant", "gram_mode", "q", "k", "m_prime", "sigma_prime", "table_bits",
-                                        "probes", "direct", "roll", "pack2")},
+                                        "probes", "direct", "roll", "pack2", "warps",
+                                        "predicted_candidates_per_byte", "measured_candidates_per_byte")},
             "params": "reference-default exact codes (restated tuner, balanced map)" if kw else "GPU planner"}
         del d, prep, eng, flush
         torch.cuda.empty_cache()
@@ -355,7 +366,8 @@ def main():
     maxlen = max(len(p) for p in w.patterns)
     # this rank's read span of the N-copy text: its own copy + the next copy's first maxlen-1 bytes
     span = w.text if rank == world - 1 else np.concatenate([w.text, w.text[:maxlen - 1]])
-    eng = mag.Engine(w.patterns, device=local)
+    # the planner prices its finalist plans by candidate rates measured on a text sample
+    eng = mag.Engine(w.patterns, device=local, histogram_sample=w.text[:1 << 20])
     plan = eng.plan()
     d_text = torch.from_numpy(span).to(f"cuda:{local}")
     prep = eng.prepare_device(d_text.data_ptr(), span.size, keep=d_text)
@@ -404,6 +416,14 @@ def main():
     kernel_ms_total, kernel_launches = mag.scan_timer_read()
     mag.scan_timer(False)
     launches = mag.kernel_launches() - launches0
+    # the dominant kernel alone (roofline): the same searches with the end
+    # event between the scan kernel and the finish grid
+    mag.scan_timer(True, scan_only=True)
+    for _ in range(args.steps):
+        eng.search_prepared_async(prep, stream.cuda_stream).close()
+    torch.cuda.synchronize()
+    scan_ms_total, scan_launches = mag.scan_timer_read()
+    mag.scan_timer(False)
     t = torch.tensor([ms], device=f"cuda:{local}")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -445,7 +465,8 @@ def main():
         return
 
     peak, peak_src = peaks()
-    kernel_ms = kernel_ms_total / max(kernel_launches, 1)
+    search_ms = kernel_ms_total / max(kernel_launches, 1)  # scan kernel + finish grid
+    kernel_ms = scan_ms_total / max(scan_launches, 1)       # scan kernel alone
     achieved = n / (kernel_ms * 1e-3) / 1e9
     traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -481,15 +502,23 @@ def main():
                    else "input smaller than L2 (not flushed)",
                    "plan": {k: plan[k] for k in ("variant", "gram_mode", "q", "k", "m_prime", "table_bits",
                                                  "entry_bits", "verify_all", "prefilter_bits", "tile_bytes",
-                                                 "warps", "stages", "smem_bytes")},
+                                                 "warps", "stages", "smem_bytes", "direct", "roll", "probes",
+                                                 "predicted_candidates_per_byte",
+                                                 "measured_candidates_per_byte", "measured_sample_bytes",
+                                                 "predicted_cost", "measured_cost", "measured_plans")},
                    "matches": n_matches, "job_matches": total_matches, "filter_reads": metrics.filter_reads,
                    "candidates": metrics.candidates, "checked_vs_reference_ac": checked,
                    "bit_exact_vs_reference_digest": digest_ok},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                      "peak_source": peak_src, "kernel_ms": kernel_ms, "algorithmic_bytes_per_launch": n,
-                     "kernel": f"mag_{plan_kernel(plan)}_kernel + mag_finish_kernel (one search = these two "
-                               "launches; CUDA events around them on the launch stream)"},
+                     "kernel": f"mag_{plan_kernel(plan)}_kernel (CUDA events around it on the launch stream, "
+                               f"{scan_launches} launches after the value region)",
+                     "search_kernels_ms": search_ms,
+                     "search_kernels_frac": n / (search_ms * 1e-3) / 1e9 / peak,
+                     "search_kernels": "scan kernel + mag_finish_kernel (one search = these two launches), "
+                                       "timed inside the value region",
+                     "step_frac": value / world / peak},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": int(span.size), "d2h_bytes_per_step": d2h,
                 "api": "mag_search (pinned host text) + clip + rank-ordered gather"},

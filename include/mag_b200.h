@@ -85,6 +85,10 @@ typedef struct mag_plan_info {
   double predicted_cost;  /* planner cost, thread-instructions per text byte (analytic rate) */
   double measured_cost;   /* the same cost re-priced with the measured rate */
   uint32_t measured_plans; /* finalist plans (one per kernel family) measured on the sample */
+  /* direct plans: filter hits per byte that also pass the L2 screen, and the
+   * bucket entries those survivors walk (entries sharing their key); -1 otherwise */
+  double measured_survivors_per_byte;
+  double measured_walk_per_byte;
 } mag_plan_info;
 
 MAG_API mag_status mag_engine_get_plan(const mag_engine* engine, mag_plan_info* out);
@@ -116,8 +120,11 @@ MAG_API mag_status mag_engine_copy_masks(const mag_engine* engine, uint64_t* out
                                          size_t count);
 MAG_API uint64_t mag_kernel_launches(void);
 
-/* Device timing of the fused scan kernel: when enabled, every scan launch is
- * bracketed by CUDA events on its stream; read() waits for and sums them. */
+/* Device timing of a search's kernels: when enabled, every scan launch is
+ * bracketed by CUDA events on its stream; read() waits for and sums them.
+ * on = 1: the scan kernel and the finish grid that follows it (one search);
+ * on = 2: the scan kernel alone (the end event is recorded between the two,
+ * so the finish grid no longer overlaps the scan's tail: timing runs only). */
 MAG_API void mag_scan_timer_enable(int on);
 MAG_API mag_status mag_scan_timer_read(double* total_ms, uint64_t* launches);
 

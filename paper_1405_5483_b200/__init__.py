@@ -93,6 +93,7 @@ class _Plan(C.Structure):  # mag_b200.h mag_plan_info
         ("pack2", C.c_int), ("measured_candidates_per_byte", C.c_double),
         ("measured_sample_bytes", C.c_uint64), ("predicted_cost", C.c_double),
         ("measured_cost", C.c_double), ("measured_plans", C.c_uint32),
+        ("measured_survivors_per_byte", C.c_double), ("measured_walk_per_byte", C.c_double),
     ]
 
 
@@ -436,9 +437,10 @@ def version() -> str:
     return lib().mag_version().decode()
 
 
-def scan_timer(enable: bool) -> None:
-    """Bracket every scan-kernel launch with CUDA events (bench/profiling)."""
-    lib().mag_scan_timer_enable(1 if enable else 0)
+def scan_timer(enable, scan_only: bool = False) -> None:
+    """Bracket every search's kernels with CUDA events (bench/profiling):
+    the scan kernel + finish grid, or with scan_only the scan kernel alone."""
+    lib().mag_scan_timer_enable((2 if scan_only else 1) if enable else 0)
 
 
 def scan_timer_read():

@@ -103,6 +103,7 @@ constexpr size_t kMaxLaunch = kMaxLaunches;
 struct ScanTimer {
   std::mutex mu;
   bool on = false;
+  bool scan_only = false;  // mode 2: the end event sits between the scan kernel and the finish grid
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spare;
   double total_ms = 0;
@@ -124,8 +125,9 @@ cudaError_t timed_launch(const ScanArgs& a, cudaStream_t st, int grid) {
     }
   }
   cudaEventRecord(ev.first, st);
-  cudaError_t e = launch_scan(a, st, grid);
-  cudaEventRecord(ev.second, st);
+  const bool scan_only = g_timer.scan_only;
+  cudaError_t e = launch_scan(a, st, grid, scan_only ? ev.second : nullptr);
+  if (!scan_only) cudaEventRecord(ev.second, st);
   std::lock_guard<std::mutex> g(g_timer.mu);
   g_timer.pending.push_back(ev);
   return e;
@@ -730,6 +732,8 @@ MAG_API mag_status mag_engine_get_plan(const mag_engine* e, mag_plan_info* out) 
   out->predicted_cost = P.pred_cost;
   out->measured_cost = P.meas_cand_per_byte < 0 ? P.pred_cost : P.meas_cost;
   out->measured_plans = P.meas_plans;
+  out->measured_survivors_per_byte = P.meas_surv_per_byte;
+  out->measured_walk_per_byte = P.meas_walk_per_byte;
   return MAG_OK;
 }
 
@@ -1065,6 +1069,7 @@ MAG_API uint64_t mag_kernel_launches(void) { return kernel_launch_count(); }
 MAG_API void mag_scan_timer_enable(int on) {
   std::lock_guard<std::mutex> g(g_timer.mu);
   g_timer.on = on != 0;
+  g_timer.scan_only = on == 2;
   g_timer.total_ms = 0;
   g_timer.launches = 0;
   for (auto& ev : g_timer.pending) g_timer.spare.push_back(ev);

@@ -257,6 +257,7 @@ constexpr double kCostSample = 30, kCostShift = 3, kCostCand = 30, kCostStart = 
 // per-sample filter work scales the same way, and one direct-kernel filter
 // hit (L2 screen load + deferred resolve) costs ~120.
 constexpr double kStagedScale = 4, kStagedFloor = 15;
+constexpr double kCostWalkEntry = 1500;  // a verification entry walked beyond the survivor's first
 double staged_scale(double model) { return kStagedScale * model + kStagedFloor; }
 
 // Expected pattern-table entries sharing a probed key (exact byte compares)
@@ -1140,19 +1141,51 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
   }
 }
 
-double measure_candidates_per_byte(const Plan& P, const std::vector<uint8_t>& table,
-                                   const uint8_t* text, size_t n) {
+FilterRates measure_filter(const Plan& P, const PatternData& pd, const std::vector<uint8_t>& table,
+                           const uint8_t* text, size_t n) {
   const ScanPlan& sp = P.sp;
-  if (n == 0) return 0;
-  uint64_t cands = 0;
-  const uint32_t* w32 = reinterpret_cast<const uint32_t*>(table.data());
+  FilterRates R;
+  if (n == 0) return R;
   if (sp.verify_all) {
-    return 1.0;
-  } else if (sp.pack2) {  // level 1: the first 10 symbols' code
+    R.candidates = 1.0;
+    return R;
+  }
+  // Verification keys of the plan (build_pattern_table), sorted: a candidate
+  // whose key is among them is a survivor, and walks every entry sharing it.
+  const bool wkey = sp.window_key != 0;
+  const unsigned klen = sp.direct ? sp.q : (wkey ? sp.wkey_len : sp.key_len);
+  std::vector<uint32_t> keys;
+  {
+    const unsigned shifts = wkey ? sp.q : 1;
+    keys.reserve(pd.r * shifts);
+    for (size_t i = 0; i < pd.r; ++i)
+      for (unsigned s = 0; s < shifts; ++s)
+        keys.push_back(sp.key_gram ? hash_gram_bytes(pd.pattern(i) + s, sp.q)
+                       : sp.pack2  ? pack2_code(pd.pattern(i), sp.q, sp.pack_shift)
+                                   : key_bytes(pd.pattern(i) + s, klen));
+    std::sort(keys.begin(), keys.end());
+  }
+  uint64_t cands = 0, surv = 0, walked = 0;
+  // a candidate whose verification key is read at text offset a
+  auto verify_at = [&](uint64_t a) {
+    if (a + klen > n) return;
+    const uint32_t key = sp.key_gram ? hash_gram_bytes(text + a, sp.q)
+                         : sp.pack2  ? pack2_code(text + a, sp.q, sp.pack_shift)
+                                     : key_bytes(text + a, klen);
+    const auto range = std::equal_range(keys.begin(), keys.end(), key);
+    if (range.first == range.second) return;
+    ++surv;
+    walked += static_cast<uint64_t>(range.second - range.first);
+  };
+  const uint32_t* w32 = reinterpret_cast<const uint32_t*>(table.data());
+  if (sp.pack2) {  // level 1: the first 10 symbols' code
     const unsigned sym = kPack2L1Bits / 2;
     for (size_t p = 0; p + sym <= n; ++p) {
       const uint32_t c = pack2_code(text + p, sym, sp.pack_shift);
-      cands += (w32[c >> 5] >> (c & 31)) & 1u;
+      if ((w32[c >> 5] >> (c & 31)) & 1u) {
+        ++cands;
+        verify_at(p);
+      }
     }
   } else if (sp.roll) {  // every position's q-byte prefix hash against its Bloom word
     const uint32_t bq = roll_pow(sp.q);
@@ -1162,7 +1195,10 @@ double measure_candidates_per_byte(const Plan& P, const std::vector<uint8_t>& ta
       bool hit = true;
       for (unsigned j = 0; j < sp.probes; ++j)
         hit = hit && ((wd >> (31u - (roll_probe_shift(h, static_cast<int>(j)) & 31u))) & 1u);
-      cands += hit;
+      if (hit) {
+        ++cands;
+        verify_at(p);
+      }
       if (p + sp.q < n) h = h * kRollB + text[p + sp.q] - text[p] * bq;
     }
   } else {
@@ -1185,38 +1221,24 @@ double measure_candidates_per_byte(const Plan& P, const std::vector<uint8_t>& ta
         mv = mask_entry(P, table, gram_index_host(P, g));
       }
       d = ((d << 1) & keep) | mv;
-      cands += static_cast<uint64_t>(__builtin_popcountll(~d & sp.match_mask));
-    }
-  }
-  return static_cast<double>(cands) / static_cast<double>(n);
-}
-
-double measure_survivors_per_byte(const Plan& P, const PatternData& pd, const std::vector<uint8_t>& table,
-                                  const uint8_t* text, size_t n) {
-  const ScanPlan& sp = P.sp;
-  if (!sp.direct || n == 0) return 0;
-  // the screen of build_pattern_table: one bit per (pattern, shift) gram key
-  std::vector<uint32_t> screen(sp.l2_bits ? std::max<size_t>(4, (size_t(1) << sp.l2_bits) / 32) : 0, 0);
-  if (sp.l2_bits)
-    for (size_t i = 0; i < pd.r; ++i)
-      for (unsigned s = 0; s < sp.q; ++s) {
-        const uint32_t b = screen_bit(hash_gram_bytes(pd.pattern(i) + s, sp.q), sp.l2_bits);
-        screen[b >> 5] |= 1u << (b & 31);
+      for (uint64_t hits = ~d & sp.match_mask; hits; hits &= hits - 1) {
+        ++cands;
+        const unsigned j = static_cast<unsigned>(__builtin_ctzll(hits)) / sp.m_prime;
+        const uint64_t back = j + static_cast<uint64_t>(sp.m_prime - 1) * sp.k;
+        if (u < back) continue;
+        const uint64_t ss = u - back;  // the candidate's super start (filter.hpp:66-70)
+        if (sp.overlapping || wkey) {
+          verify_at(sp.overlapping ? ss : ss * sp.q);  // one start / one window key at the gram boundary
+        } else {  // start keys: every start of the window [q ss - (q - 1), q ss]
+          for (uint64_t s = 0; s < sp.q && s <= ss * sp.q; ++s) verify_at(ss * sp.q - s);
+        }
       }
-  uint64_t surv = 0;
-  for (uint64_t t = 0; t < n / sp.q; ++t) {
-    const uint32_t h = hash_gram_bytes(text + t * sp.q, sp.q);
-    bool hit = true;
-    if (sp.probes > 1) {
-      for (unsigned i = 0; i < sp.probes; ++i) hit = hit && !(mask_entry(P, table, probe_entry(sp, h, i)) & 1ull);
-    } else {
-      hit = !(mask_entry(P, table, gram_slot(h, sp.table_bits)) & 1ull);
     }
-    if (!hit) continue;
-    const uint32_t b = screen_bit(h, sp.l2_bits);
-    surv += sp.l2_bits ? (screen[b >> 5] >> (b & 31)) & 1u : 1u;
   }
-  return static_cast<double>(surv) / static_cast<double>(n);
+  R.candidates = static_cast<double>(cands) / static_cast<double>(n);
+  R.survivors = static_cast<double>(surv) / static_cast<double>(n);
+  R.walked = static_cast<double>(walked) / static_cast<double>(n);
+  return R;
 }
 
 int make_plan_measured(const PatternData& pd, const Histogram& h, const PlanRequest& rq,
@@ -1227,13 +1249,19 @@ int make_plan_measured(const PatternData& pd, const Histogram& h, const PlanRequ
   auto measure = [&](Plan* pl) {
     std::vector<uint8_t> table;
     build_masks(*pl, pd, &table);
-    pl->meas_cand_per_byte = measure_candidates_per_byte(*pl, table, sample, n);
+    const FilterRates fr = measure_filter(*pl, pd, table, sample, n);
+    pl->meas_cand_per_byte = fr.candidates;
+    pl->meas_surv_per_byte = fr.survivors;
+    pl->meas_walk_per_byte = fr.walked;
     pl->meas_sample_bytes = n;
     double cost = pl->pred_cost + pl->cost_slope * (pl->meas_cand_per_byte - pl->pred_cand_per_byte);
-    if (pl->sp.direct) {
-      pl->meas_surv_per_byte = measure_survivors_per_byte(*pl, pd, table, sample, n);
-      cost += pl->surv_slope * (pl->meas_surv_per_byte - pl->pred_surv_per_byte);
-    }
+    // direct plans price the survivors of the L2 screen separately
+    if (pl->sp.direct) cost += pl->surv_slope * (pl->meas_surv_per_byte - pl->pred_surv_per_byte);
+    // every family: entries walked beyond one per survivor cost a serial L2
+    // round trip each, in one lane of the warp (B200: word-Zipf text whose
+    // survivors walk ~300 entries ran the direct kernel at 1 GB/s, i.e.
+    // ~1,500 per walked entry in this unit)
+    cost += kCostWalkEntry * std::max(0.0, pl->meas_walk_per_byte - pl->meas_surv_per_byte);
     pl->meas_cost = std::max(0.0, cost);
   };
   measure(P);

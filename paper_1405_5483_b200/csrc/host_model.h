@@ -97,9 +97,13 @@ struct Plan {
   // the candidate rate: a measured rate re-prices the plan as
   // pred_cost + cost_slope * (measured - predicted)
   double pred_cost = 0, cost_slope = 0;
-  // direct plans: filter hits that also pass the L2 screen walk a bucket
-  // (true gram matches of repetitive text all do); priced separately
+  // survivors: candidates whose verification key is a pattern's (true gram
+  // matches of repetitive text); direct plans price them separately.  Each
+  // survivor walks every table entry sharing its key, one dependent L2 round
+  // trip per entry in a single lane: repetitive text whose grams occur in
+  // hundreds of patterns (SURVEY.md §7 hard part 2)
   double pred_surv_per_byte = 0, surv_slope = 0, meas_surv_per_byte = -1;
+  double meas_walk_per_byte = -1;
   // measured on a text sample (mag_options.histogram_sample): -1 = no sample
   double meas_cand_per_byte = -1, meas_cost = 0;
   uint64_t meas_sample_bytes = 0;
@@ -122,14 +126,15 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
 int make_plan_measured(const PatternData& pd, const Histogram& h, const PlanRequest& rq,
                        const uint8_t* sample, size_t sample_len, Plan* plan, std::string* err);
 
-// The plan's own filter over text[0, n): candidates per text byte, counted
-// as the kernels count mag_metrics.candidates.
-double measure_candidates_per_byte(const Plan& plan, const std::vector<uint8_t>& table,
-                                   const uint8_t* text, size_t n);
-// Direct plans: filter hits per byte that also pass the L2 screen bitmap
-// (built here from the patterns' (pattern, shift) gram keys).
-double measure_survivors_per_byte(const Plan& plan, const PatternData& pd, const std::vector<uint8_t>& table,
-                                  const uint8_t* text, size_t n);
+// The plan's own filter and verification keys over text[0, n), per text
+// byte: candidates as the kernels count mag_metrics.candidates; survivors =
+// candidates whose verification key is a pattern's; walked = the table entries
+// those survivors visit (all entries sharing the key).
+struct FilterRates {
+  double candidates = 0, survivors = 0, walked = 0;
+};
+FilterRates measure_filter(const Plan& plan, const PatternData& pd, const std::vector<uint8_t>& table,
+                           const uint8_t* text, size_t n);
 
 // Packed mask table (bit j*m'+i of entry c is 0 iff c admitted at alignment
 // j position i; filter.hpp:27-31), table_bytes long.

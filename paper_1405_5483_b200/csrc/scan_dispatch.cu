@@ -200,8 +200,9 @@ cudaError_t launch_scan_only(const ScanArgs& a, cudaStream_t stream, int grid) {
 }
 }  // namespace
 
-cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid) {
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid, cudaEvent_t after_scan) {
   cudaError_t e = launch_scan_only(a, stream, grid);
+  if (after_scan) cudaEventRecord(after_scan, stream);
   if (e != cudaSuccess || !a.final_launch) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(a.finish_grid);

@@ -98,7 +98,9 @@ struct LaunchShape {
 // Enqueues the fused filter + verify kernel (persistent, `grid` CTAs); after
 // the search's final launch, the finish grid (programmatic dependent) that
 // places the slices' matches in order and publishes the counters.
-cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid);
+// `after_scan` (timing only) is recorded between the scan kernel and the
+// finish grid; the finish grid then starts after the scan has completed.
+cudaError_t launch_scan(const ScanArgs& a, cudaStream_t stream, int grid, cudaEvent_t after_scan = nullptr);
 
 // SMAG prepare: codes[u] = mask index of gram u, for u < n/q.
 cudaError_t launch_encode(const ScanPlan& plan, const uint8_t* text, uint64_t n,

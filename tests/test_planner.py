@@ -1,0 +1,192 @@
+"""GPU-aware parameter choice with measured candidate rates.
+
+The reference's cost model (tuner.hpp:58-66) predicts the
+filter's pass rate from a uniform-text model.  Given a text sample
+(mag_options.histogram_sample, mag.h:59-70) the engine instead runs the
+finalist plans' own filters, with their real tables, over up to 1 MiB of it
+and prices the plans with the measured rates (host_model.cpp
+make_plan_measured).  These tests pin the measurement against the restated
+machine's counters (oracle) and show the uniform model's error on Zipf text.
+"""
+import numpy as np
+import pytest
+
+
+
+def rand_instance(rng, sig, n, r, m, base):
+    """iid text over `sig` symbols; half of the patterns (length m..m+4) copied from it."""
+    text = (rng.integers(0, sig, n) + base).astype(np.uint8)
+    pats = []
+    for _ in range(r):
+        L = m + int(rng.integers(0, 5))
+        if rng.random() < 0.5:
+            s = int(rng.integers(0, n - L + 1))
+            pats.append(text[s:s + L].tobytes())
+        else:
+            pats.append((rng.integers(0, sig, L) + base).astype(np.uint8).tobytes())
+    return text, pats
+
+
+def zipf_words_text(rng, n_words=200_000, vocab=500):
+    """Word-level Zipf(1.0) text: a few hundred words repeated, space separated."""
+    words = [bytes(rng.integers(97, 123, size=int(rng.integers(2, 9))).astype(np.uint8)) + b" "
+             for _ in range(vocab)]
+    p = 1.0 / np.arange(1, vocab + 1)
+    p /= p.sum()
+    ids = rng.choice(vocab, size=n_words, p=p)
+    return np.frombuffer(b"".join(words[i] for i in ids), dtype=np.uint8)
+
+
+def copied(rng, text, r, m):
+    return [text[o:o + m].tobytes() for o in rng.integers(0, text.size - m, size=r)]
+
+
+def test_no_sample_reports_no_measurement(mag):
+    rng = np.random.default_rng(1)
+    text, pats = rand_instance(rng, sig=4, n=20000, r=50, m=20, base=65)
+    pl = mag.Engine(pats, device=-2).plan()
+    assert pl["measured_candidates_per_byte"] == -1.0
+    assert pl["measured_sample_bytes"] == 0 and pl["measured_plans"] == 0
+    assert pl["measured_cost"] == pl["predicted_cost"]
+    # a sample below 4 KiB is only used for the histogram
+    pl = mag.Engine(pats, device=-2, histogram_sample=text[:1000]).plan()
+    assert pl["measured_candidates_per_byte"] == -1.0
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(scan_kernel="staged"), dict(scan_kernel="roll"),
+                                dict(q=3, k=1, sigma_prime=4, mapping="balance"),
+                                dict(variant="shiftor_og", q=4), dict(scan_kernel="direct", probes=3)])
+def test_measured_rate_equals_restated_machine(mag, port, kw):
+    """measured_candidates_per_byte * sample bytes == the candidates the
+    restated filter machine (filter.hpp:58-73, oracle/mag_oracle.c) counts on
+    the same bytes with the same parameters."""
+    from pyoracle import roll_candidates
+    rng = np.random.default_rng(7)
+    text, pats = rand_instance(rng, sig=4, n=60000, r=200, m=33, base=65)
+    e = mag.Engine(pats, device=-2, histogram_sample=text, **kw)
+    pl = e.plan()
+    assert pl["measured_sample_bytes"] == text.size and pl["measured_plans"] >= 1
+    got = round(pl["measured_candidates_per_byte"] * text.size)
+    if pl["roll"]:
+        want = roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, pl["probes"])
+    elif pl["gram_mode"] == 0:
+        info = e.info()
+        table, sp = e.alphabet()
+        P = port.params(variant=0 if pl["variant"] == 0 else 2, gram_mode=0, q=info.q, k=info.k, sigma_prime=sp,
+                        table=table)
+        want = port.search(text, pats, P)[3]
+    else:
+        P = port.params(variant=0 if pl["variant"] == 0 else 2, gram_mode=1, q=pl["q"], k=pl["k"],
+                        table_bits=pl["table_bits"], word_bits=pl["k"] * pl["m_prime"], probes=pl["probes"],
+                        blocks=pl["blocks"])
+        want = port.search(text, pats, P)[3]
+    assert got == want, pl
+
+
+def test_uniform_model_underestimates_zipf_text(mag):
+    """Patterns copied from word-Zipf text: the text's grams repeat the
+    patterns' grams, which the uniform model cannot see (SURVEY.md §7 hard
+    part 2); the measured rate is an order of magnitude above the prediction
+    and the plan's cost is re-priced with it."""
+    rng = np.random.default_rng(5)
+    text = zipf_words_text(rng)
+    pats = copied(rng, text, 2000, 16)
+    pl = mag.Engine(pats, device=-2, histogram_sample=text).plan()
+    assert pl["measured_sample_bytes"] == min(text.size, 1 << 20)
+    assert pl["measured_plans"] >= 2  # the finalists of several kernel families were measured
+    assert pl["measured_candidates_per_byte"] > 8 * pl["predicted_candidates_per_byte"], pl
+    assert pl["measured_cost"] > pl["predicted_cost"]
+    # iid text of the same alphabet: the model holds (within 25%)
+    flat = rng.integers(97, 123, size=text.size).astype(np.uint8)
+    pats2 = [bytes(rng.integers(97, 123, size=16).astype(np.uint8)) for _ in range(2000)]
+    pl2 = mag.Engine(pats2, device=-2, histogram_sample=flat).plan()
+    assert abs(pl2["measured_candidates_per_byte"] / pl2["predicted_candidates_per_byte"] - 1) < 0.25, pl2
+
+
+def test_pinned_plans_are_measured_not_replaced(mag):
+    rng = np.random.default_rng(9)
+    text = zipf_words_text(rng, 60_000)
+    pats = copied(rng, text, 300, 20)
+    for kw in (dict(scan_kernel="staged"), dict(q=2, k=2), dict(scan_kernel="roll")):
+        a = mag.Engine(pats, device=-2, **kw).plan()
+        b = mag.Engine(pats, device=-2, histogram_sample=text, **kw).plan()
+        same = ("q", "k", "m_prime", "table_bits", "probes", "direct", "roll", "variant", "gram_mode")
+        assert {k: a[k] for k in same} == {k: b[k] for k in same}
+        assert b["measured_plans"] == 1 and b["measured_candidates_per_byte"] >= 0
+
+
+def test_measured_choice_leaves_the_direct_kernel_on_repetitive_text(mag):
+    """Word-Zipf text whose grams occur in hundreds of patterns: every filter
+    hit of an aligned-sample plan is a true gram match that walks all the
+    (pattern, shift) entries sharing its key.  The analytic planner picks the
+    direct kernel (B200: 1 GB/s on this shape); with the sample the walk is
+    measured and the whole-prefix rolling scan is chosen (54 GB/s).  The
+    BASELINE.json shapes keep their calibrated plans."""
+    from paper_1405_5483_b200 import workloads
+    rng = np.random.default_rng(3)
+    text = zipf_words_text(rng, 300_000, 200)
+    pats = copied(rng, text, 5000, 24)
+    a = mag.Engine(pats, device=-2).plan()
+    b = mag.Engine(pats, device=-2, histogram_sample=text).plan()
+    assert a["direct"] == 1 and a["roll"] == 0
+    assert b["roll"] == 1 and b["direct"] == 0 and b["measured_plans"] >= 3, b
+    d = mag.Engine(pats, device=-2, histogram_sample=text, scan_kernel="direct").plan()
+    assert d["measured_walk_per_byte"] > 20 * d["measured_survivors_per_byte"] > 0  # long walks per survivor
+    assert d["measured_cost"] > 10 * b["measured_cost"]
+    for cfg, scale in ((1, 1.0), (2, 1 / 64), (3, 1 / 32), (4, 1 / 64), (5, 1 / 64)):
+        w = workloads.generate(cfg, scale)
+        p0 = mag.Engine(w.patterns, device=-2).plan()
+        p1 = mag.Engine(w.patterns, device=-2, histogram_sample=w.text[:1 << 20]).plan()
+        same = ("q", "k", "m_prime", "table_bits", "probes", "direct", "roll", "variant", "gram_mode", "warps")
+        assert {k: p0[k] for k in same} == {k: p1[k] for k in same}, cfg
+        assert p1["measured_walk_per_byte"] <= 1.5 * p1["measured_survivors_per_byte"] + 1e-9
+
+
+@pytest.mark.gpu
+def test_measured_choice_is_faster_on_the_gpu(mag, ref):
+    """The same shape on the GPU: both plans return the reference's match set;
+    the measured choice (roll) is several times faster than the analytic one
+    (direct) — a 50x gap at full size, asserted here as 3x on 12 MiB."""
+    import torch
+    from pyoracle import as_pairs
+    rng = np.random.default_rng(3)
+    text = zipf_words_text(rng, 2_000_000, 200)
+    pats = copied(rng, text, 5000, 24)
+    want = as_pairs(*ref.ac(text, pats, threads=8))
+    d = torch.from_numpy(text.copy()).cuda()
+    times = {}
+    for label, kw in (("analytic", {}), ("measured", dict(histogram_sample=text[:1 << 20]))):
+        e = mag.Engine(pats, **kw)
+        p = e.prepare_device(d.data_ptr(), d.numel(), keep=d)
+        m = e.search_prepared(p)
+        assert m.pairs() == want, label
+        m.close()
+        s = torch.cuda.Stream()
+        e.search_prepared_async(p, s.cuda_stream).close()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        e.search_prepared_async(p, s.cuda_stream).close()
+        e1.record(s)
+        torch.cuda.synchronize()
+        times[label] = (e0.elapsed_time(e1), e.plan())
+    assert times["analytic"][1]["direct"] == 1 and times["measured"][1]["roll"] == 1
+    assert times["analytic"][0] > 3 * times["measured"][0], {k: v[0] for k, v in times.items()}
+
+
+@pytest.mark.gpu
+def test_measured_rate_predicts_the_kernel_counter(mag, ref):
+    """On the GPU: candidates / n of a real search stays within 15% of the
+    rate measured on the first 1 MiB, on Zipf text where the analytic
+    prediction is off by more than 8x; the match set is the reference's."""
+    from pyoracle import as_pairs
+    rng = np.random.default_rng(11)
+    text = zipf_words_text(rng, 600_000)
+    pats = copied(rng, text, 2000, 16)
+    e = mag.Engine(pats, histogram_sample=text[:1 << 20])
+    pl = e.plan()
+    m = e.search(text)
+    assert m.pairs() == as_pairs(*ref.ac(text, pats))
+    rate = m.metrics().candidates / text.size
+    assert abs(rate / pl["measured_candidates_per_byte"] - 1) < 0.15, (rate, pl)
+    assert rate > 8 * pl["predicted_candidates_per_byte"]
