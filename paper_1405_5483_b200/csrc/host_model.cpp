@@ -572,7 +572,9 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       // measured W = 16 at 13/14/15/16 warps: cfg4 2,551/2,604/2,686/1,934
       // GB/s (a 16th scanning warp leaves L1 ~17 KB for the screen and bucket
       // loads), cfg2 15 vs 16 = 4,802 vs 4,689 GB/s.
-      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps) : kMaxWarps - 1;
+      // Round 2, W = 8: 16 warps 3,428 vs 15 warps 3,317 GB/s on cfg3.
+      const uint32_t warps = rq.warps > 0 ? std::min<uint32_t>(rq.warps, kMaxWarps)
+                                          : (q == 8 ? kMaxWarps : kMaxWarps - 1);
       // ring depth: multi-probe tables run 4-deep rings; single-probe q = 16
       // tables default to 2-deep rings, whose freed 32 KB doubles the table
       // (2^20 bits: measured +4% cfg2, +16% cfg4 over 4-deep / 2^19)

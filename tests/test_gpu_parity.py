@@ -384,6 +384,43 @@ def test_roll_kernel(mag, ref, H):
             assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[5:], pats))
 
 
+@pytest.mark.parametrize("m,H,warps", [(8, 1, 0), (9, 2, 0), (10, 3, 0), (12, 3, 0), (12, 3, 20), (11, 3, 24)])
+def test_roll_kernel_equal_short_sets(mag, ref, m, H, warps):
+    """The roll kernel's path for equal-length sets of m <= 12 bytes (cfg5's
+    shape): 1 KiB steps, two-entry verification sectors, verification
+    pipelined across steps.  Covers texts around the step and slice sizes,
+    q < m (starts past n - m), dense steps (> 64 and > 128 candidates: the
+    rank-search expansion), duplicate patterns (two matches in one sector)
+    and overflowing home sectors (>= 3 identical patterns: the walk)."""
+    from pyoracle import roll_candidates
+    rng = np.random.default_rng(100 * m + H)
+    sizes = [0, m - 1, m, 1023, 1024, 1025, 1024 + m, 32768 + 5, 70001, 250000]
+    for it, n in enumerate(sizes):
+        sig = [2, 4, 4, 20][it % 4]
+        text = (rng.integers(0, sig, n) + 65).astype(np.uint8)
+        r = int(rng.integers(1, 400))
+        pats = []
+        for _ in range(r):
+            if n > m and rng.random() < 0.6:
+                s0 = int(rng.integers(0, n - m + 1))
+                pats.append(text[s0:s0 + m].tobytes())
+            else:
+                pats.append((rng.integers(0, sig, m) + 65).astype(np.uint8).tobytes())
+        pats += [pats[0]] * 4  # five identical patterns: their home sector overflows
+        if n >= m:
+            pats.append(text[n - m:n].tobytes())  # ends at n
+        text = text.copy()
+        if it % 2 == 1 and n > 4096:  # a dense stretch: every position of 3 KiB starts a match
+            text[1000:4072] = np.frombuffer(pats[0], dtype=np.uint8)[0]
+            pats.append(bytes([pats[0][0]]) * m)
+        e = mag.Engine(pats, scan_kernel="roll", probes=H, warps=warps)
+        pl = e.plan()
+        assert pl["roll"] == 1 and pl["tile_bytes"] == 1024, pl
+        got, met = gpu_pairs(e, text)
+        assert got == as_pairs(*ref.ac(text, pats)), (n, m, sig, pl)
+        assert met.candidates == roll_candidates(text, pats, pl["q"], pl["table_bytes"] // 4, H), (n, m)
+
+
 def test_concurrent_searches_one_engine(mag, ref):
     """An engine is immutable and searches on it may run concurrently
     (engine.hpp:55-56): host threads searching different texts through one
