@@ -299,7 +299,9 @@ def config_sweep(cells, local, steps=10, warmup=3):
             "plan": {k: pl[k] for k in ("variant", "gram_mode", "q", "k", "m_prime", "sigma_prime", "table_bits",
                                         "probes", "direct", "roll", "pack2", "warps",
                                         "predicted_candidates_per_byte", "measured_candidates_per_byte")},
-            "params": "reference-default exact codes (restated tuner, balanced map)" if kw else "GPU planner"}
+            "params": ("GPU planner" if not kw else
+                       "reference-default exact codes (analytic-seed q/k of SURVEY 8a, balanced map)" if "q" in kw
+                       else "reference-default exact codes (restated tuner's joint q/k, balanced map)")}
         del d, prep, eng, flush
         torch.cuda.empty_cache()
     return out
@@ -485,6 +487,10 @@ def main():
             if c != args.config:
                 cells.append((c, "", {}))
             cells.append((c, "_reference_params", {"gram_mode": 0}))
+        # SURVEY 8a's other reading of the bodiless tuner (analytic seeds, no joint grid)
+        for c, q, k in ((1, 5, 1), (3, 3, 1), (5, 6, 1)):
+            cells.append((c, "_analytic_seed_params", {"gram_mode": 0, "q": q, "k": k}))
+        cells.sort(key=lambda x: x[0])
         sweep = config_sweep(cells, local)
     cpu = None
     if not args.no_cpu_baseline and world == 1:

@@ -336,6 +336,28 @@ def test_full_configs_reference_params(mag, port, cfg):
     assert match_digest(offs, pids) == want["matches_sha256"], (cfg, pl)
 
 
+@pytest.mark.parametrize("cfg,q,k,mp", [(1, 5, 1, 2), (3, 3, 1, 4), (5, 6, 1, 1)])
+def test_full_configs_analytic_seed_params(mag, cfg, q, k, mp):
+    """SURVEY.md §8a's other reading of the (bodiless) tuner: the analytic
+    seeds q = round(log_sigma'(rm)) and k without the joint grid
+    (tuner.hpp:44-56), which differ from the restated joint choice on cfg1
+    (q = 5, m' = 2), cfg3 (q = 3, m' = 4) and cfg5 (q = 6).  Exact codes,
+    balanced map; the same full-size digests."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    from make_full_digests import match_digest
+    from paper_1405_5483_b200 import workloads
+    want = _full_digests()[str(cfg)]
+    w = workloads.generate(cfg, 1.0)
+    e = mag.Engine(w.patterns, gram_mode=mag.GRAM_EXACT, q=q, k=k)
+    pl, info = e.plan(), e.info()
+    assert (pl["gram_mode"], info.q, info.k, pl["m_prime"], info.mapping) == (0, q, k, mp, mag.MAPPING_BALANCED)
+    offs, pids = e.search(w.text).arrays()
+    assert offs.size == want["matches"], (cfg, pl)
+    assert match_digest(offs, pids) == want["matches_sha256"], (cfg, pl)
+
+
 @pytest.mark.parametrize("H", [2, 3])
 def test_roll_kernel(mag, ref, H):
     """The dense rolling-hash scan (forced): every template q, unequal and

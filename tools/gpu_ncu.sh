@@ -5,7 +5,7 @@
 # $KEEP_REP's .ncu-rep is kept (gpurun copies back <= 64 MiB).
 mkdir -p gpurun_out
 if [ -z "$SKIP_LAUNCHES" ]; then
-B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1"
+B="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 --headline-only"
 $B > gpurun_out/plain_bench.log 2>&1 &&
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_cfg2.csv $B > gpurun_out/ncu_launches.log 2>&1
