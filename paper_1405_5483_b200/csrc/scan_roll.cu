@@ -286,11 +286,16 @@ struct RollScanner {
 
   __device__ __forceinline__ void consume() {
     if (pend_n == 0) return;
+    const bool two = pend_n > 32;  // warp-uniform: the lanes' second candidates exist (20% of cfg5's steps)
     pend_n = 0;
     bool hit0[2], hit1[2];
     bool slow = false;
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if (k == 1 && !two) {
+        hit0[1] = hit1[1] = false;
+        continue;
+      }
       const bool live = pend_pr[k] != 0xffffffffu;
       hit0[k] = live && entry_is(pend_e0[k], pend_tx[k][0], pend_tx[k][1], pend_tx[k][2]);
       hit1[k] = live && entry_is(pend_e1[k], pend_tx[k][0], pend_tx[k][1], pend_tx[k][2]);
@@ -300,6 +305,7 @@ struct RollScanner {
     if (!__any_sync(kFull, slow)) {  // the common case: at most one match, decided by the home sector
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
+        if (k == 1 && !two) continue;
         const bool hit = hit0[k] || hit1[k];
         const unsigned one = __ballot_sync(kFull, hit);
         if (hit) {
@@ -314,6 +320,7 @@ struct RollScanner {
     // count (home sector + the walk), then place in (start, pid) order
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if (k == 1 && !two) continue;
       const bool live = pend_pr[k] != 0xffffffffu;
       const bool go = live && pend_e0[k].w != 0xffffffffu && (pend_e0[k].w >> 31);
       const unsigned long long a = pend_t + pend_pr[k];
@@ -341,8 +348,14 @@ struct RollScanner {
   __device__ __forceinline__ void request(const uint32_t* sw, uint32_t base, uint32_t total, bool listed,
                                           uint32_t h, uint32_t excl, int tail) {
     uint32_t key[2];
+    const bool two = total - base > 32;  // warp-uniform
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if (k == 1 && !two) {
+        pend_pr[1] = 0xffffffffu;
+        key[1] = 0;
+        continue;
+      }
       const uint32_t rank = base + 32 * k + lane;
       bool live = rank < total;
       uint32_t pr;
@@ -373,6 +386,7 @@ struct RollScanner {
     // lanes without a candidate read sector 0
 #pragma unroll
     for (int k = 0; k < 2; ++k) {
+      if (k == 1 && !two) continue;
       const uint32_t sec = pend_pr[k] != 0xffffffffu ? key[k] & A.vmask : 0u;
       pend_e0[k] = __ldg(A.vtab + 2 * sec);
       pend_e1[k] = __ldg(A.vtab + 2 * sec + 1);
