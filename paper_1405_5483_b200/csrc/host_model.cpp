@@ -1060,10 +1060,13 @@ void build_pattern_table(const Plan& P, const PatternData& pd, PatternTable* pt)
     // its home sector while that has room (id order: entry 0 before entry
     // 1); pass 2 moves the others to the next sector with room and sets F
     // in the HOME sector's entry 0: "patterns of this home live further
-    // along" — the only case in which the kernel walks on (~1.6% of the
-    // patterns at <= 0.25 patterns per sector).
+    // along" — the only case in which the kernel walks on (~0.4% of the
+    // patterns at <= 0.125 patterns per sector).
     size_t sectors = 16;
-    while (sectors < 4 * r) sectors <<= 1;
+    // cfg5 (r = 100k), sectors >= 4r / 8r / 16r: 774 / 805 / 812 GB/s (fewer
+    // overflowing home sectors, hence fewer walks); 8r = 32 MiB stays a
+    // quarter of L2
+    while (sectors < (r <= (size_t(1) << 20) ? 8 : 4) * r) sectors <<= 1;
     pt->vmask = static_cast<uint32_t>(sectors - 1);
     pt->vtab.assign(8 * sectors, 0);
     for (size_t i = 0; i < 2 * sectors; ++i) pt->vtab[4 * i + 3] = 0xffffffffu;
