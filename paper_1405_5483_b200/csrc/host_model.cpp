@@ -1160,7 +1160,9 @@ FilterRates measure_filter(const Plan& P, const PatternData& pd, const std::vect
   const bool wkey = sp.window_key != 0;
   const unsigned klen = sp.direct ? sp.q : (wkey ? sp.wkey_len : sp.key_len);
   std::vector<uint32_t> keys;
-  {
+  // (sets beyond 2^25 keys are measured for candidates only: no key index)
+  const bool index_keys = pd.r * (wkey ? sp.q : 1u) <= (size_t(1) << 25);
+  if (index_keys) {
     const unsigned shifts = wkey ? sp.q : 1;
     keys.reserve(pd.r * shifts);
     for (size_t i = 0; i < pd.r; ++i)
@@ -1173,7 +1175,7 @@ FilterRates measure_filter(const Plan& P, const PatternData& pd, const std::vect
   uint64_t cands = 0, surv = 0, walked = 0;
   // a candidate whose verification key is read at text offset a
   auto verify_at = [&](uint64_t a) {
-    if (a + klen > n) return;
+    if (!index_keys || a + klen > n) return;
     const uint32_t key = sp.key_gram ? hash_gram_bytes(text + a, sp.q)
                          : sp.pack2  ? pack2_code(text + a, sp.q, sp.pack_shift)
                                      : key_bytes(text + a, klen);
