@@ -34,6 +34,15 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
   // clear the other half of the group sums for the next search
   for (uint64_t i = blockIdx.x * kFinishThreads + tid; i < A.group_sum_words; i += uint64_t(gridDim.x) * kFinishThreads)
     A.group_sum_next[i] = 0;
+  // Requested before the prefix is known (independent loads, one round trip
+  // together with the prefix's): the first chunk's group sums and this warp's
+  // first group's slice counts.
+  const unsigned long long gs_first = g0 + tid < g1 ? A.group_sum[g0 + tid] : 0ull;
+  uint32_t cnt_first = 0;
+  if (g0 + wid < g1) {
+    const uint64_t x = (g0 + wid) * kGroup + lane;
+    cnt_first = x < A.num_slices ? A.slice_count[x] : 0u;
+  }
   // matches before g0
   unsigned long long acc = 0;
   for (uint64_t i = tid; i < g0; i += kFinishThreads) acc += A.group_sum[i];
@@ -47,7 +56,7 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
   for (uint64_t c0 = g0; c0 < g1; c0 += kFinishThreads) {
     // block scan of this chunk's group sums
     const uint64_t g = c0 + tid;
-    const unsigned long long gs = g < g1 ? A.group_sum[g] : 0ull;
+    const unsigned long long gs = c0 == g0 ? gs_first : (g < g1 ? A.group_sum[g] : 0ull);
     unsigned long long v = gs;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -68,7 +77,8 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
       const uint64_t grp = c0 + k;
       const unsigned long long gb = s_base[k];
       const uint64_t x = grp * kGroup + lane;
-      const uint32_t cnt = x < A.num_slices ? A.slice_count[x] : 0u;
+      const uint32_t cnt = (c0 == g0 && k == static_cast<uint64_t>(wid)) ? cnt_first
+                                                                         : (x < A.num_slices ? A.slice_count[x] : 0u);
       uint32_t u = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
