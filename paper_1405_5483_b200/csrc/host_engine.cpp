@@ -253,11 +253,15 @@ uint64_t step_unit(const Plan& P) {
 
 // Slices are the warps' work items: the plan's size, but small texts get
 // smaller slices (whole kernel steps) so that every warp of the grid has
-// about four of them.
+// one (direct plans) or two of them: each slice costs a ticket, a TMA ramp
+// and an exposed screen round trip at its end.
 uint64_t slice_samples_for(const mag_engine* e, uint64_t samples) {
   const Plan& P = e->plan;
   const uint64_t unit = step_unit(P);
-  const uint64_t warps = static_cast<uint64_t>(e->sm_count) * P.nwarps * 4;
+  // B200, slices per warp 4 / 2 / 1: cfg1 (16 MiB, direct) 420 / 489 / 539 GB/s per step,
+  // cfg2 at 64 MiB 1,572 / 1,613 / 1,734; cfg5 at 32 MiB (roll) 438 / 449 / 405
+  const uint64_t per_warp = P.sp.direct ? 1 : 2;
+  const uint64_t warps = static_cast<uint64_t>(e->sm_count) * P.nwarps * per_warp;
   uint64_t want = (samples + warps - 1) / warps;
   want = (want + unit - 1) / unit * unit;
   return std::max<uint64_t>(unit, std::min<uint64_t>(P.slice_samples, want));
