@@ -30,8 +30,8 @@ typedef struct mag_options_ex {
   int table_bits;  /* hashed: log2 mask entries; 0 = auto; -1 = no filter (verify all) */
   int word_bits;   /* w of the reference machine (filter.hpp:34); 0 = 64 */
   int tile_bytes;  /* 0 = auto */
-  int warps;       /* scanning warps per CTA, 0 = auto (<= 15 staged / W=16 direct, <= 16 W=8 / roll);
-                      every CTA adds one gather warp */
+  int warps;       /* warps per scan CTA, 0 = auto (15 staged / W=16 direct, 16 W=8 direct / roll;
+                      up to 24 for the roll kernel's equal-length short-set path) */
   int stages;      /* TMA ring depth, 0 = auto */
   int device;      /* CUDA device ordinal, -1 = current */
   int probes;      /* hashed: table entries probed per gram, 0 = auto */

@@ -306,8 +306,8 @@ class Engine:
     sigma_prime, threads, histogram_sample) plus the GPU extras of
     ``mag_options_ex`` (gram_mode, table_bits, word_bits, tile_bytes, warps,
     stages, device, probes, scan_kernel; device=-2 builds the host tables
-    only, no upload).  ``warps`` counts scanning warps; every CTA adds one
-    gather warp.
+    only, no upload).  ``histogram_sample`` of >= 4 KiB of text also lets the
+    planner measure its finalist plans' candidate rates on it.
     """
 
     def __init__(self, patterns: Sequence[bytes], variant="mag", mapping="auto", lowbits=0, q=0, k=0,

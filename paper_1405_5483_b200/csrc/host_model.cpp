@@ -206,7 +206,7 @@ namespace {
 constexpr uint32_t kChunkTarget = 1536;   // gram bytes per ring slot
 constexpr uint32_t kSliceTarget = 32768;  // text bytes per warp work item
 constexpr uint32_t kDefaultRing = 2;
-constexpr uint32_t kDefaultWarps = kMaxWarps - 1;  // scanning warps; the CTA adds its gather warp
+constexpr uint32_t kDefaultWarps = kMaxWarps - 1;  // staged plans: 15 warps (calibrated in round 1)
 
 unsigned pow2ceil_log2(unsigned x) {
   unsigned l = 0;
@@ -568,8 +568,7 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
       if (!((rq.kernel == 0 || rq.kernel == 2) && rq.table_bits >= 0 && !sp.overlapping && m >= 2 * q - 1 &&
             (rq.q == 0 || rq.q == static_cast<int>(q)) && rq.k <= 1 && depth_ok && rq.tile_bytes == 0))
         continue;
-      // 15 scanning warps + the CTA's gather warp.  Round 1 (no gather warp)
-      // measured W = 16 at 13/14/15/16 warps: cfg4 2,551/2,604/2,686/1,934
+      // Round 1 measured W = 16 at 13/14/15/16 warps: cfg4 2,551/2,604/2,686/1,934
       // GB/s (a 16th scanning warp leaves L1 ~17 KB for the screen and bucket
       // loads), cfg2 15 vs 16 = 4,802 vs 4,689 GB/s.
       // Round 2, W = 8: 16 warps 3,428 vs 15 warps 3,317 GB/s on cfg3.

@@ -186,7 +186,7 @@ struct ScanPlan {
 
 // ---- shared-memory layout of the scan kernel (host computes the size,
 // device carves it; one definition for both).
-constexpr int kMaxWarps = 16;   // launch bound: 512 threads; scans launch at most 15 warps (the 16th's registers host the gather grid)
+constexpr int kMaxWarps = 16;   // launch bound: 512 threads (the roll kernel's equal-length path: up to kRollMaxWarps)
 constexpr int kQueueCap = 64;   // candidate windows queued per warp (per chunk)
 constexpr int kProbeCap = 128;  // window keys awaiting the L2 screen (per slice)
 constexpr int kHitWords = 32;   // per-chunk hit bitmap (chunks of <= 1024 samples, k = 1)

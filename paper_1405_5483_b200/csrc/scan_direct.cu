@@ -7,7 +7,7 @@
 // L2 screen word is loaded at once and resolved a step later, survivors
 // queue per warp, walk their (pattern, shift) bucket and are compared against
 // the text in global memory.  Output: per-slice ordered staging, placed by
-// the CTA's gather warp (kern_common.cuh).
+// the finish grid (scan_dispatch.cu).
 //
 // Replaces FilterMachine::scan_range (filter.hpp:51-74) + verify_window
 // (verify.hpp:28-31) for these plans; the match set is the reference's.
@@ -282,8 +282,7 @@ struct DirectScanner {
   }
 };
 
-// NT: launch bound (15 warps are launched: the 16th warp's registers host
-// the search's gather kernel).
+// NT: launch bound (512 threads; W = 16 plans launch 15 warps, W = 8 plans 16).
 template <int H, int DEPTH, int NT, int W>
 __global__ void __launch_bounds__(NT, 1) mag_direct_kernel(const __grid_constant__ ScanArgs A) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -329,8 +328,7 @@ cudaError_t launch_direct_hd(const ScanArgs& a, cudaStream_t stream, int grid, s
 
 template <int H>
 cudaError_t launch_direct_h(const ScanArgs& a, cudaStream_t stream, int grid, size_t smem) {
-  // 15 warps per CTA: the gather kernel's one-warp CTAs take the 16th
-  // warp's registers (a 17th warp would cut every warp to 96 registers)
+  // at most 16 warps per CTA (a 17th would cut every warp to 96 registers)
   if (a.plan.q == 8) {  // 8-byte samples (m >= 15)
     if constexpr (H <= 4) return launch_direct_hd<H, kDirectDepth, 512, 8>(a, stream, grid, smem);
     return cudaErrorInvalidValue;

@@ -80,7 +80,7 @@ MAG_HD uint64_t slice_t1(const ScanArgs& a, uint64_t x) {
 
 // Control words of one search (a half of the workspace's ctrl array).
 // Each group has its own 128-byte line, so the scanning warps' ticket
-// atomics never share a line with the gather warps' polls.
+// atomics never share a line with the finish grid's counters.
 constexpr unsigned kCtrTotal = 1;      // total matches (finish grid)
 constexpr unsigned kCtrExits = 16;     // finish CTAs that have left
 constexpr unsigned kCtrCands = 32;     // filter candidates

@@ -302,8 +302,7 @@ struct Pack2Scanner {
   }
 };
 
-// 15 warps are launched (the 16th warp's registers host the finish grid's
-// CTAs as the scan drains)
+// launch bound: 512 threads (15 warps are launched)
 constexpr int kPack2Threads = 16 * 32;
 
 __global__ void __launch_bounds__(kPack2Threads, 1) mag_pack2_kernel(const __grid_constant__ ScanArgs A) {

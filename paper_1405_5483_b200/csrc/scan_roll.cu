@@ -20,7 +20,7 @@ namespace {
 // (warp prefix over the masks) and verified while the step is still staged:
 // start key of the candidate's first min(m,16) bytes -> bucket walk ->
 // byte compare against the staged text.  Output: per-slice ordered staging,
-// as every other scan kernel (mag_compact_kernel gathers).
+// as every other scan kernel (mag_finish_kernel places the slices in order).
 struct __align__(16) RollDesc {
   unsigned long long t;  // first position (= byte offset) of the step
   uint32_t slice;
@@ -591,7 +591,6 @@ struct RollScanner {
   }
 };
 
-// launch bound: 15 warps are launched (the gather kernel takes the 16th's registers)
 // NT: launch bound (512; 640 / 768 for the EQ kernel's 20- / 24-warp CTAs)
 template <int Q, int H, bool EQ, int NT>
 __global__ void __launch_bounds__(NT, 1) mag_roll_kernel(const __grid_constant__ ScanArgs A) {
