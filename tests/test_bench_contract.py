@@ -1,0 +1,81 @@
+"""The bench line's contract (task statement section 4 and SURVEY.md 8d),
+checked on the committed round evidence (profiles/r02_bench.json is the line
+`bench.py --steps 20 --warmup 5` printed on a B200) and on bench.py's source:
+every required key is present, the roofline fraction is achieved / peak with
+the scan kernel no slower than the whole step, every config row is
+digest-checked, and the product never measures the oracle."""
+import json
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _line():
+    with open(os.path.join(ROOT, "profiles", "r02_bench.json")) as f:
+        return json.load(f)
+
+
+def test_required_keys_and_types():
+    d = _line()
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["unit"] == "GB/s" and d["dtype"] == "u8" and d["data"] == "synthetic" and d["higher_is_better"] is True
+    assert d["vs_baseline"] is None  # BASELINE.md holds no published number for this metric on this hardware
+    assert d["config"]["workload"].startswith("cfg2-") and "model" not in d["config"]
+    assert d["warmup"] >= 3 and d["n_gpus"] == 1 and d["scaling"] == "weak"
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    c = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in c, k
+    assert c["kind"] in ("reference", "port") and c["same_config"] is True
+    e = d["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["h2d_bytes_per_step"] == d["config"]["n"] and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 2 * d["steps"]  # scan kernel + finish grid per search
+    assert not set(d["clocks"]["reasons"]) & {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
+
+
+def test_roofline_is_consistent():
+    d = _line()
+    r, n = d["roofline"], d["config"]["n"]
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    assert abs(r["achieved"] - n / (r["kernel_ms"] * 1e-3) / 1e9) < 1e-6 * r["achieved"]
+    assert r["algorithmic_bytes_per_launch"] == n
+    # the scan kernel is part of the search, the search part of the step
+    assert r["kernel_ms"] < r["search_kernels_ms"] < d["ms_per_step"]
+    assert abs(d["value"] - n / (d["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * d["value"]
+    assert 0.5 < r["step_frac"] < r["search_kernels_frac"] < r["frac"] < 1.0  # north_star: >= 50% of HBM on cfg2
+    assert 1.0 <= r["traffic"] / n < 1.05 and "static" in r["traffic_source"]
+    assert d["e2e"]["value"] < d["value"]  # host buffers: PCIe bound
+
+
+def test_every_config_row_is_bit_exact_and_named():
+    rows = _line()["configs"]
+    for c in (1, 3, 4, 5):
+        assert f"cfg{c}" in rows
+    for c in (1, 2, 3, 4, 5):
+        assert f"cfg{c}_reference_params" in rows
+        assert rows[f"cfg{c}_reference_params"]["plan"]["gram_mode"] == 0  # the reference's exact codes
+    for name, row in rows.items():
+        assert row["bit_exact_vs_reference"] is True, name
+        assert row["scan_kernel_GB/s"] >= row["kernel_GB/s"] * 0.999 >= row["GB/s"] * 0.99, name
+    assert rows["cfg2_reference_params"]["plan"]["m_prime"] == 3  # the paper's multi-position filter
+    assert rows["cfg1_analytic_seed_params"]["plan"]["m_prime"] == 2
+
+
+def test_bench_source_uses_the_oracle_only_as_baseline():
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    # oracle/ is imported only by the CPU baseline legs and the optional --check
+    uses = [m.start() for m in re.finditer(r"from pyoracle import", src)]
+    assert uses, "bench.py lost its CPU baseline"
+    for u in uses:
+        head = src[:u]
+        fn = re.findall(r"\ndef (\w+)\(", head)[-1]
+        assert fn in ("cpu_reference", "mag_restated_baseline", "main"), fn
+    assert "/root/reference" not in src
