@@ -18,15 +18,14 @@ std::atomic<unsigned long long> g_launches{0};
 // sum of the group sums before g0 (a coalesced pass over at most a few
 // thousand words) and a block scan of its own give each group's base; a warp
 // per group scans the group's 32 slice counts and copies the group's matches
-// as one flat run, 8 loads in flight per lane.  The last CTA out publishes
-// the counters and clears the next search's control words.
+// as one flat run, 16 loads in flight per lane.  The CTA of the last groups
+// publishes the counters and clears the next search's control words.
 constexpr int kFinishThreads = 512;
 __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid_constant__ ScanArgs A) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) diag_time(A, 2, true);
   __shared__ unsigned long long red[kFinishThreads / 32];
   __shared__ unsigned long long s_base[kFinishThreads];  // inclusive sums of the owned groups (this chunk)
-  __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int kW = kFinishThreads / 32;
   const uint64_t G = (A.num_slices + kGroup - 1) / kGroup;
@@ -127,19 +126,16 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
     base += ctot;
     __syncthreads();
   }
-  // the block of the last groups knows the total; the last CTA out publishes
-  if (blockIdx.x == gridDim.x - 1 && tid == 0) A.counters[kCtrTotal] = base;
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(A.counters + kCtrExits, 1ull) + 1 == gridDim.x;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+  // The CTA of the last groups knows the total.  It publishes the counters
+  // and clears the NEXT search's control words (the other parity half, which
+  // no CTA of this search reads), so it need not wait for the other CTAs:
+  // the kernel's completion orders everything before the next search.
+  if (blockIdx.x != gridDim.x - 1) return;
   if (tid == 0) {
     const volatile unsigned long long* c = A.counters;
     volatile unsigned long long* h = A.host_ctr;
     h[1] = c[kCtrCands];
-    h[2] = c[kCtrTotal];
+    h[2] = base;
     h[3] = c[kCtrMax];
   }
   if ((A.plan.diag & 2048) && tid < 4) {  // diagnostics timeline
