@@ -144,9 +144,7 @@ __global__ void __launch_bounds__(kFinishThreads) mag_finish_kernel(const __grid
     const uint64_t t = tid == 2 ? global_ns() : (tid == 1 ? ~c[kCtrTime + 2] : c[kCtrTime + 1 + tid]);
     A.host_ctr[4 + tid] = t - t0;
   }
-  __syncthreads();
   for (uint32_t i = tid; i < A.reset_words; i += kFinishThreads) A.reset[i] = 0;
-  __threadfence_system();
 }
 
 // SMAG prepare (encode_text qgram.cpp:29-37) on the device.
