@@ -120,7 +120,7 @@ def test_measured_choice_leaves_the_direct_kernel_on_repetitive_text(mag):
     hit of an aligned-sample plan is a true gram match that walks all the
     (pattern, shift) entries sharing its key.  The analytic planner picks the
     direct kernel (B200: 1 GB/s on this shape); with the sample the walk is
-    measured and the whole-prefix rolling scan is chosen (54 GB/s).  The
+    measured and the whole-prefix rolling scan is chosen (45 GB/s).  The
     BASELINE.json shapes keep their calibrated plans."""
     from paper_1405_5483_b200 import workloads
     rng = np.random.default_rng(3)
