@@ -326,7 +326,6 @@ def as_pairs(offs, pids):
 # reference algorithm: paper_1405_5483_b200/csrc/mag_common.h roll_*), used
 # to check the roll kernel's Bloom table and its candidate counter.
 ROLL_B = 0x9E3779B1
-ROLL_MIX = 0x2C1B3C6D
 
 
 def roll_hashes(text, q: int) -> np.ndarray:
@@ -346,8 +345,7 @@ ROLL_PROBE_MUL = {1: 0x85EBCA77, 2: 0xC2B2AE3D}
 
 
 def _roll_slots(h: np.ndarray, words: int, probes: int):
-    with np.errstate(over="ignore"):
-        g = h.astype(np.uint32) * np.uint32(ROLL_MIX)
+    g = h.astype(np.uint32)  # the hash itself picks the word (top bits) and probe 0 (low bits)
     w = ((g.astype(np.uint64) * np.uint64(words)) >> np.uint64(32)).astype(np.int64)
     shifts = [g] + [((h.astype(np.uint64) * np.uint64(ROLL_PROBE_MUL[i])) >> np.uint64(32)).astype(np.uint32)
                     for i in range(1, probes)]

@@ -949,7 +949,7 @@ void build_masks(const Plan& P, const PatternData& pd, std::vector<uint8_t>* tab
     uint32_t* w = reinterpret_cast<uint32_t*>(table->data());
     for (size_t i = 0; i < pd.r; ++i) {
       const uint32_t h = roll_hash_bytes(pd.pattern(i), sp.q);
-      const uint32_t wi = roll_word(h * kRollMix, sp.roll_words);
+      const uint32_t wi = roll_word(h, sp.roll_words);
       for (unsigned j = 0; j < sp.probes; ++j)
         w[wi] |= 1u << (31u - (roll_probe_shift(h, static_cast<int>(j)) & 31u));
     }
@@ -1197,7 +1197,7 @@ FilterRates measure_filter(const Plan& P, const PatternData& pd, const std::vect
     const uint32_t bq = roll_pow(sp.q);
     uint32_t h = n >= sp.q ? roll_hash_bytes(text, sp.q) : 0;
     for (size_t p = 0; p + sp.q <= n; ++p) {
-      const uint32_t wd = w32[roll_word(h * kRollMix, sp.roll_words)];
+      const uint32_t wd = w32[roll_word(h, sp.roll_words)];
       bool hit = true;
       for (unsigned j = 0; j < sp.probes; ++j)
         hit = hit && ((wd >> (31u - (roll_probe_shift(h, static_cast<int>(j)) & 31u))) & 1u);

@@ -120,16 +120,14 @@ struct RollScanner {
 
   // Bloom probe bits sit at 31 - (s_i & 31) (mag_common.h roll_probe_shift),
   // so rotl(word, s_i) (funnel shift, wrap mode: the count is taken mod 32)
-  // brings each to bit 31; their AND's bit 31 is the verdict.  s_0 = g and
+  // brings each to bit 31; their AND's bit 31 is the verdict.  s_0 = h and
   // s_i = umulhi(h, C_i): the extra probes cost fma-pipe IMAD.HIs, not
   // alu-pipe shifts.
   __device__ __forceinline__ uint32_t test(uint32_t h) const {
-    const uint32_t g = h * kRollMix;
-    // word address by IMAD (fma pipe; the alu pipe is the busier one)
     uint32_t addr, wd;
-    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(roll_word(g, A.plan.roll_words)), "r"(bloom_s));
+    asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(addr) : "r"(roll_word(h, A.plan.roll_words)), "r"(bloom_s));
     asm("ld.shared.u32 %0, [%1];" : "=r"(wd) : "r"(addr));
-    uint32_t r = __funnelshift_l(wd, wd, g);
+    uint32_t r = __funnelshift_l(wd, wd, h);
 #pragma unroll
     for (int i = 1; i < H; ++i) r &= __funnelshift_l(wd, wd, __umulhi(h, roll_probe_mul(i)));
     return r;  // verdict in bit 31
