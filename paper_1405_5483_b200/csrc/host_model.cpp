@@ -821,7 +821,10 @@ int make_plan(const PatternData& pd, const Histogram& h, const PlanRequest& rq, 
     P->slice_samples = 32768;  // whole steps either way
     P->back = best_halo;
     P->ring = kRollDepth;
+    // more than 16 warps: only the 3-probe equal-length kernels are built with
+    // the wider launch bounds (scan_roll.cu launch_roll_qhe)
     P->nwarps = best_roll_warps ? best_roll_warps : kMaxWarps - 1;
+    if (sp.probes != 3) P->nwarps = std::min<uint32_t>(P->nwarps, kMaxWarps);
   }
 
   // ---- shared-memory placement

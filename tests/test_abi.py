@@ -215,6 +215,17 @@ def test_product_never_imports_the_oracle():
                     assert not re.search(bad, src), (f, bad)
 
 
+def test_roll_warps_follow_the_built_kernels(mag):
+    """More than 16 warps exist only for the 3-probe equal-length roll kernels
+    (scan_roll.cu launch_roll_qhe); other plans clamp the request."""
+    pats = [b"ACGTACGTAC", b"ACGTTTGTAC", b"TTGTACGTAC"]
+    for H, w, want in ((3, 24, 24), (3, 20, 20), (2, 24, 16), (1, 20, 16), (3, 0, 16)):
+        pl = mag.Engine(pats, scan_kernel="roll", probes=H, warps=w, device=-2).plan()
+        assert pl["warps"] == want and pl["smem_bytes"] <= 232448, (H, w, pl)
+    unequal = pats + [b"ACGTACGTACGTA"]
+    assert mag.Engine(unequal, scan_kernel="roll", warps=24, device=-2).plan()["warps"] == 16
+
+
 def test_roll_bloom_equals_restatement(mag):
     """Forced roll plans: the uploaded Bloom words equal the restated filter
     (oracle/pyoracle.py roll_bloom) for every template q."""

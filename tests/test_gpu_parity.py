@@ -406,7 +406,8 @@ def test_roll_kernel(mag, ref, H):
             assert e.search_prepared(pd).pairs() == as_pairs(*ref.ac(text[5:], pats))
 
 
-@pytest.mark.parametrize("m,H,warps", [(8, 1, 0), (9, 2, 0), (10, 3, 0), (12, 3, 0), (12, 3, 20), (11, 3, 24)])
+@pytest.mark.parametrize("m,H,warps", [(8, 1, 0), (9, 2, 0), (10, 3, 0), (12, 3, 0), (12, 3, 20), (11, 3, 24),
+                                       (10, 2, 24)])  # 2-probe kernels are built for <= 16 warps: the plan clamps
 def test_roll_kernel_equal_short_sets(mag, ref, m, H, warps):
     """The roll kernel's path for equal-length sets of m <= 12 bytes (cfg5's
     shape): 1 KiB steps, two-entry verification sectors, verification
