@@ -47,10 +47,11 @@ def test_roofline_is_consistent():
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
     assert abs(r["achieved"] - n / (r["kernel_ms"] * 1e-3) / 1e9) < 1e-6 * r["achieved"]
     assert r["algorithmic_bytes_per_launch"] == n
-    # the scan kernel is part of the search, the search part of the step
-    assert r["kernel_ms"] < r["search_kernels_ms"] < d["ms_per_step"]
+    # the scan kernel is part of the step, and of the (event-serialised) search
+    assert r["kernel_ms"] < d["ms_per_step"] and r["kernel_ms"] < r["search_kernels_serialized_ms"]
     assert abs(d["value"] - n / (d["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * d["value"]
-    assert 0.5 < r["step_frac"] < r["search_kernels_frac"] < r["frac"] < 1.0  # north_star: >= 50% of HBM on cfg2
+    assert 0.5 < r["step_frac"] < r["frac"] < 1.0  # north_star: >= 50% of HBM on cfg2
+    assert r["search_kernels_serialized_frac"] < r["frac"]
     assert 1.0 <= r["traffic"] / n < 1.05 and "static" in r["traffic_source"]
     assert d["e2e"]["value"] < d["value"]  # host buffers: PCIe bound
 
@@ -64,7 +65,8 @@ def test_every_config_row_is_bit_exact_and_named():
         assert rows[f"cfg{c}_reference_params"]["plan"]["gram_mode"] == 0  # the reference's exact codes
     for name, row in rows.items():
         assert row["bit_exact_vs_reference"] is True, name
-        assert row["scan_kernel_GB/s"] >= row["kernel_GB/s"] * 0.999 >= row["GB/s"] * 0.99, name
+        assert row["scan_kernel_GB/s"] == row["kernel_GB/s"] >= row["GB/s"] * 0.99, name
+        assert row["scan_kernel_GB/s"] >= row["search_kernels_serialized_GB/s"] * 0.999, name
     assert rows["cfg2_reference_params"]["plan"]["m_prime"] == 3  # the paper's multi-position filter
     assert rows["cfg1_analytic_seed_params"]["plan"]["m_prime"] == 2
 
